@@ -1,0 +1,84 @@
+/*
+ * maxsim_b200.h -- C-ABI of the B200-native Flash-MaxSim operator.
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument is a DEVICE pointer unless stated otherwise; the caller owns
+ *     every buffer (no allocation happens inside the library except cached TMA descriptors
+ *     on the host stack);
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered and returns
+ *     as soon as the work is enqueued;
+ *   - the return value is an mxs_status; MXS_OK == 0.  mxs_last_error() returns a
+ *     thread-local human-readable message for the most recent failure on this thread.
+ *   - status codes map 1:1 onto the reference's typed errors (maxsim/errors.py:8-78).
+ *
+ * Each entry point cites the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src).
+ */
+#ifndef MAXSIM_B200_H
+#define MAXSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MXS_OK = 0,
+  MXS_DIM_MISMATCH = 1,       /* maxsim/errors.py:13 DimMismatch */
+  MXS_SHAPE_MISMATCH = 2,     /* maxsim/errors.py:35 ShapeMismatch */
+  MXS_EMPTY_DOCUMENT = 3,     /* maxsim/errors.py:29 EmptyDocument */
+  MXS_INDEX_OUT_OF_RANGE = 4, /* maxsim/errors.py:43 IndexOutOfRange */
+  MXS_STALE_CSR = 5,          /* maxsim/errors.py:47 StaleCsr */
+  MXS_K_TOO_LARGE = 6,        /* maxsim/errors.py:55 KTooLarge */
+  MXS_NAN_INPUT = 7,          /* maxsim/errors.py:21 NaNInput */
+  MXS_BAD_TILE_CONFIG = 8,    /* maxsim/errors.py:39 BadTileConfig */
+  MXS_UNSUPPORTED = 9,        /* shape/dtype outside what the sm_100a kernels accept */
+  MXS_CUDA_ERROR = 10,        /* launch or driver failure */
+  MXS_INVALID_ARGUMENT = 11   /* null pointer / negative size */
+} mxs_status;
+
+typedef enum { MXS_F32 = 0, MXS_F16 = 1, MXS_BF16 = 2, MXS_I8 = 3 } mxs_dtype;
+
+/* Library identification. */
+const char* mxs_version(void);
+const char* mxs_status_string(int status);
+const char* mxs_last_error(void);
+/* Number of SMs of the current device (grid sizing), or -1 on error. */
+int mxs_device_sm_count(void);
+
+/*
+ * Dense all-pairs forward.  Replaces maxsim/forward.py:221 fused_score_batch (and
+ * maxsim/forward.py:158 fused_score_pair for n_q = n_docs = 1).
+ *   Q          [n_q, l_q, dim]        elements of `dtype`
+ *   D          [n_docs, l_pad, dim]   zero-padded documents (maxsim/types.py:80 DocBatch)
+ *   valid_lens [n_docs] int32, or NULL for "all rows valid"; every entry in [1, l_pad]
+ *   scores     [n_q, n_docs] float64  (S4: sequential f64 sum of fp32 row maxima)
+ *   argmax     [n_q, n_docs, l_q] int32, document-local, lowest index on ties; may be NULL
+ *   rowmax     [n_q, n_docs, l_q] float32 scratch/output (the per-token maxima)
+ *   exact      0: tcgen05 tensor-core path (MXS_BF16 / MXS_F16; fp32 accumulation)
+ *              1: bit-exact fp32 fold on CUDA cores (S1; any float dtype, required for MXS_F32)
+ */
+int mxs_fused_score_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
+                          int64_t l_pad, int64_t dim, const int32_t* valid_lens, double* scores, int32_t* argmax,
+                          float* rowmax, int exact, void* stream);
+
+/*
+ * INT8 x INT8 dense forward with fused dequantisation.  Replaces maxsim/quant.py:128
+ * fused_score_int8 (batched over documents and queries; the reference is per pair).
+ *   Q [n_q, l_q, dim] int8, q_scale [n_q, l_q] f32; D [n_docs, l_pad, dim] int8,
+ *   d_scale [n_docs, l_pad] f32.  sim = fl(fl(f32(int32 acc) * s_q) * s_d)  (S7).
+ */
+int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int64_t l_q, const int8_t* D,
+                         const float* d_scale, int64_t n_docs, int64_t l_pad, int64_t dim, const int32_t* valid_lens,
+                         double* scores, int32_t* argmax, float* rowmax, void* stream);
+
+/* Sequential f64 row sum (S4) of rowmax [n_pairs, l_q] into scores [n_pairs]. */
+int mxs_rowsum(const float* rowmax, int64_t n_pairs, int64_t l_q, double* scores, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAXSIM_B200_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of libmaxsim_b200.so (include/maxsim_b200.h).
+
+The library is the only compute path: if it is missing or fails to load, every operator
+raises.  There is no CPU or PyTorch fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+from ._build import LIB_PATH
+
+_lock = threading.Lock()
+_lib = None
+
+c_int = ctypes.c_int
+c_i64 = ctypes.c_int64
+c_vp = ctypes.c_void_p
+c_dbl = ctypes.c_double
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+_SIGNATURES = {
+    "mxs_version": [],
+    "mxs_status_string": [c_int],
+    "mxs_last_error": [],
+    "mxs_device_sm_count": [],
+    "mxs_fused_score_batch": [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_vp],
+    "mxs_fused_score_int8": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "mxs_rowsum": [c_vp, c_i64, c_i64, c_vp, c_vp],
+}
+_RESTYPES = {
+    "mxs_version": ctypes.c_char_p,
+    "mxs_status_string": ctypes.c_char_p,
+    "mxs_last_error": ctypes.c_char_p,
+}
+
+MXS_F32, MXS_F16, MXS_BF16, MXS_I8 = 0, 1, 2, 3
+
+_STATUS_TO_ERROR = {
+    1: errors.DimMismatch,
+    2: errors.ShapeMismatch,
+    3: errors.EmptyDocument,
+    4: errors.IndexOutOfRange,
+    5: errors.StaleCsr,
+    6: errors.KTooLarge,
+    7: errors.NaNInput,
+    8: errors.BadTileConfig,
+    9: errors.Unsupported,
+    10: errors.CudaError,
+    11: errors.ShapeMismatch,
+}
+
+
+def lib_path() -> str:
+    return os.environ.get("MXS_LIB_PATH", LIB_PATH)
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises if the native library is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = lib_path()
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"libmaxsim_b200.so not found at {path}; run `python -m paper_2605_29517_b200._build` "
+                "(the operator has no CPU fallback)"
+            )
+        lib = ctypes.CDLL(path)
+        for name, args in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, c_int)
+        _lib = lib
+    return _lib
+
+
+def declared_symbols():
+    return list(_SIGNATURES)
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = load().mxs_last_error().decode(errors="replace")
+    cls = _STATUS_TO_ERROR.get(status, errors.CudaError)
+    text = f"{what}: {msg}" if what else msg
+    if hasattr(cls, "from_message"):
+        raise cls.from_message(text)
+    raise cls(text)
+
+def call(name: str, *args) -> None:
+    fn = getattr(load(), name)
+    check(fn(*args), name)

@@ -1,0 +1,150 @@
+// Bit-exact FP32 MaxSim forward on CUDA cores (K10).
+//
+// Restates the reference element arithmetic exactly (S1): every similarity is the strict
+// left-to-right fp32 fold `acc = fl(acc + fl(q_k * d_k))` of `maxsim/kernels.py:29-38`
+// (dot_block), with no FMA contraction (__fmul_rn / __fadd_rn), so scores and argmax match
+// the numpy oracle bit for bit, including ties.  Masking (S2) and the strict-> lowest-index
+// fold (S3) follow `maxsim/forward.py:146-155` and `maxsim/kernels.py:69-93`.
+//
+// One CTA folds one (query, document) pair at a time: 32 query rows x 64 document tokens per
+// sub-tile, 8 accumulators per thread, the embedding axis streamed through shared memory in
+// chunks of 128 (the fold order over k is preserved across chunks).
+#pragma once
+#include "ptx.cuh"
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+namespace mxs {
+
+struct FwdExactParams {
+  int n_q, l_q, n_docs, l_pad, dim;
+  const int32_t* valid_lens;  // nullable
+  const long long* cu_seqlens;  // packed layout when non-null (then l_pad unused)
+  float* rowmax;
+  int32_t* argmax;
+};
+
+constexpr int kExRows = 32, kExCols = 64, kExK = 64, kExThreads = 256;
+
+template <typename T>
+MXS_DEV float to_f32(T x);
+template <>
+MXS_DEV float to_f32<float>(float x) { return x; }
+template <>
+MXS_DEV float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <>
+MXS_DEV float to_f32<__half>(__half x) { return __half2float(x); }
+
+template <typename T>
+__global__ void __launch_bounds__(kExThreads) fwd_exact_kernel(const T* __restrict__ Q, const T* __restrict__ D,
+                                                                const FwdExactParams p) {
+  __shared__ float sQ[kExRows][kExK + 1];
+  __shared__ float sD[kExCols][kExK + 1];
+  __shared__ float xm[8][kExRows];
+  __shared__ int xi[8][kExRows];
+  const int tid = threadIdx.x;
+  const int i = tid & 31;   // query row within the row tile
+  const int jg = tid >> 5;  // column phase: columns jg, jg+8, ...
+  const long long n_pairs = (long long)p.n_q * p.n_docs;
+  for (long long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+    const int q = (int)(pr / p.n_docs), b = (int)(pr % p.n_docs);
+    long long drow0;
+    int vl;
+    if (p.cu_seqlens) {
+      drow0 = p.cu_seqlens[b];
+      vl = (int)(p.cu_seqlens[b + 1] - drow0);
+    } else {
+      drow0 = (long long)b * p.l_pad;
+      vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+    }
+    const T* qbase = Q + (long long)q * p.l_q * p.dim;
+    const T* dbase = D + drow0 * p.dim;
+    for (int r0 = 0; r0 < p.l_q; r0 += kExRows) {
+      float m = -INFINITY;
+      int ix = 0;
+      for (int c0 = 0; c0 < vl; c0 += kExCols) {
+        float acc[8];
+        for (int k0 = 0; k0 < p.dim; k0 += kExK) {
+          const int kw = min(kExK, p.dim - k0);
+          __syncthreads();
+          for (int e = tid; e < kExRows * kExK; e += kExThreads) {
+            const int rr = e / kExK, kk = e % kExK;
+            sQ[rr][kk] = (r0 + rr < p.l_q && kk < kw) ? to_f32(qbase[(long long)(r0 + rr) * p.dim + k0 + kk]) : 0.f;
+          }
+          for (int e = tid; e < kExCols * kExK; e += kExThreads) {
+            const int cc = e / kExK, kk = e % kExK;
+            sD[cc][kk] = (c0 + cc < vl && kk < kw) ? to_f32(dbase[(long long)(c0 + cc) * p.dim + k0 + kk]) : 0.f;
+          }
+          __syncthreads();
+          int k = 0;
+          if (k0 == 0) {
+            const float qv = sQ[i][0];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = __fmul_rn(qv, sD[jg + 8 * c][0]);
+            k = 1;
+          }
+          for (; k < kw; ++k) {
+            const float qv = sQ[i][k];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(qv, sD[jg + 8 * c][k]));
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = c0 + jg + 8 * c;
+          if (j < vl && acc[c] > m) {
+            m = acc[c];
+            ix = j;
+          }
+        }
+      }
+      xm[jg][i] = m;
+      xi[jg][i] = ix;
+      __syncthreads();
+      if (jg == 0 && r0 + i < p.l_q) {
+        float bm = xm[0][i];
+        int bi = xi[0][i];
+        for (int w = 1; w < 8; ++w) {
+          const float om = xm[w][i];
+          const int oi = xi[w][i];
+          if (om > bm || (om == bm && oi < bi)) {
+            bm = om;
+            bi = oi;
+          }
+        }
+        const long long o = ((long long)q * p.n_docs + b) * p.l_q + r0 + i;
+        p.rowmax[o] = bm;
+        if (p.argmax) p.argmax[o] = bi;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Per-pair score: strict left-to-right float64 sum of the fp32 row maxima (S4,
+// `maxsim/kernels.py:22-26` seq_sum_f64).  One warp per pair; every lane carries the same
+// running sum so the chain is sequential without divergence.
+__global__ void rowsum_kernel(const float* __restrict__ rowmax, long long n_pairs, int l_q, double* __restrict__ scores) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_pairs) return;
+  const float* r = rowmax + warp * l_q;
+  double s = 0.0;
+  bool first = true;
+  for (int c = 0; c < l_q; c += 32) {
+    const float v = (c + lane < l_q) ? r[c + lane] : 0.f;
+    const int nv = min(32, l_q - c);
+    for (int j = 0; j < nv; ++j) {
+      const double x = (double)__shfl_sync(0xffffffffu, v, j);
+      if (first) {
+        s = x;
+        first = false;
+      } else {
+        s = __dadd_rn(s, x);
+      }
+    }
+  }
+  if (lane == 0) scores[warp] = s;
+}
+
+}  // namespace mxs
