@@ -1,6 +1,7 @@
 // extern "C" entry points of libmaxsim_b200.so (see include/maxsim_b200.h).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -117,6 +118,10 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   p.d_scale = d_scale;
   p.rowmax = rowmax;
   p.argmax = argmax;
+  {
+    const char* dbg = getenv("MXS_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
   CUtensorMap tq, td;
   const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16

@@ -33,6 +33,7 @@ struct FwdTcParams {
   const float* d_scale;       // I8 only: [n_docs * l_pad]
   float* rowmax;              // [n_q, n_docs, l_q]
   int32_t* argmax;            // [n_q, n_docs, l_q] or nullptr
+  int debug;                  // profiling knobs (MXS_DEBUG env): 1 = skip fold, 2 = skip TMEM loads too
 };
 
 constexpr int kTileRows = 128;     // rows per Q block and per document tile
@@ -292,7 +293,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + slot * 128u;
           const int base = t * kTileRows;
-          if constexpr (KIND == TcKind::I8) {
+          if (p.debug) {
+            if (p.debug == 1) {
+              uint32_t ra[32], rb[32];
+              tmem_ld32(taddr, ra);
+              tmem_ld32(taddr + 32, rb);
+              tmem_ld32(taddr + 64, ra);
+              tmem_ld32(taddr + 96, rb);
+              tmem_ld_wait();
+              m[i] = fmaxf(m[i], __uint_as_float(ra[0] ^ rb[31]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+          } else if constexpr (KIND == TcKind::I8) {
             // lower register pressure: two chunks in flight at a time
             uint32_t ra[32], rb[32];
             tmem_ld32(taddr, ra);
