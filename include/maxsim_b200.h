@@ -74,8 +74,74 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
                          const float* d_scale, int64_t n_docs, int64_t l_pad, int64_t dim, const int32_t* valid_lens,
                          double* scores, int32_t* argmax, float* rowmax, void* stream);
 
+/*
+ * Padding-free forward over a packed corpus.  Replaces maxsim/varlen.py:88 fused_score_varlen
+ * (generalised to n_q queries).
+ *   tokens [n_tokens, dim] (concatenated document rows), cu_seqlens [n_docs + 1] int64 with
+ *   cu[0] = 0, strictly increasing, cu[n_docs] = n_tokens (maxsim/varlen.py:22-63).
+ *   scores [n_q, n_docs] f64; argmax [n_q, n_docs, l_q] int32 document-local; rowmax scratch.
+ */
+int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* tokens,
+                           const int64_t* cu_seqlens, int64_t n_docs, int64_t n_tokens, int64_t dim, double* scores,
+                           int32_t* argmax, float* rowmax, int exact, void* stream);
+
 /* Sequential f64 row sum (S4) of rowmax [n_pairs, l_q] into scores [n_pairs]. */
 int mxs_rowsum(const float* rowmax, int64_t n_pairs, int64_t l_q, double* scores, void* stream);
+
+/*
+ * Per-token symmetric quantisation.  Replaces maxsim/quant.py:104 quantize_per_token.
+ *   x [rows, dim] of `dtype` (f32 / bf16 / f16) -> q [rows, dim] int8, scale [rows] f32 (S7).
+ */
+int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, int levels, int8_t* q, float* scale,
+                           void* stream);
+
+/*
+ * Inverse-grid CSR of the saved argmax.  Replaces maxsim/backward.py:81 build_inverse_csr.
+ *   argmax    [n_q, n_docs, l_q] int32 document-local winners
+ *   dest_off  [n_docs] int64 first destination row of each document (maxsim/types.py:205-211:
+ *             b * padded_len for a padded batch, prefix sums of doc_lens when packed)
+ *   dest_len  [n_docs] int64 destination rows owned by each document (padded_len or doc_len)
+ *   row_ptr   [n_dest + 1] int32, col_idx [n_q * n_docs * l_q] int32 (ascending source id per
+ *             bucket, i.e. the reference's stable argsort)
+ *   ws        >= mxs_csr_workspace_bytes(n_q, n_dest) bytes of device scratch
+ */
+size_t mxs_csr_workspace_bytes(int64_t n_q, int64_t n_dest);
+int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, int64_t l_q, const int64_t* dest_off,
+                          const int64_t* dest_len, int64_t n_dest, int64_t max_dest_len, int32_t* row_ptr,
+                          int32_t* col_idx, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Destination-owned document gradient.  Replaces maxsim/backward.py:135 grad_docs_csr.
+ *   dD[r] = sum_{s in bucket r} g[q(s), b(s)] * Q[q_row(s)]   (fp32 accumulation, no atomics)
+ *   g [n_q, n_docs] f32; Q [n_q, l_q, dim] of `dtype`; dD [n_dest, dim] f32.
+ */
+int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx, int64_t n_dest, const float* g,
+                      const void* Q, int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, float* dD, void* stream);
+
+/*
+ * Query gradient (gather).  Replaces maxsim/backward.py:218 grad_query.
+ *   dQ[q, i] = sum_b g[q, b] * D[doc_row_off[b] + argmax[q, b, i]]   (b ascending, fp32)
+ *   D is the flat [rows, dim] document buffer (padded batch or packed tokens).
+ */
+int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void* D, const int64_t* doc_row_off,
+                   int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, float* dQ, void* stream);
+
+/*
+ * Top-K selection with the reference ranking: score descending, document id ascending.
+ * Replaces maxsim/streamio.py:230 TopKHeap (offer/ranked) and maxsim/cli.py:88 _ranked.
+ *   scores [n] f64 -> top_s [k] f64, top_id [k] int64 (= position + id_offset).
+ *   ws >= mxs_topk_workspace_bytes(n, k) bytes (may be NULL when n <= 8192).
+ */
+size_t mxs_topk_workspace_bytes(int64_t n, int64_t k);
+int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, double* top_s, int64_t* top_id, void* ws,
+             size_t ws_bytes, void* stream);
+/*
+ * Top-K over explicit (score, id) candidates, e.g. the all-gathered per-rank top-K lists of a
+ * sharded corpus; entries with id < 0 are empty slots.  Same ordering as mxs_topk
+ * (maxsim/streamio.py:255-262 TopKHeap.merge).  Slots beyond the valid candidates get id -1.
+ */
+int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
+                        void* stream);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ c_int = ctypes.c_int
 c_i64 = ctypes.c_int64
 c_vp = ctypes.c_void_p
 c_dbl = ctypes.c_double
+c_size = ctypes.c_size_t
 
 # name -> argtypes (restype is int unless listed in _RESTYPES)
 _SIGNATURES = {
@@ -30,11 +31,23 @@ _SIGNATURES = {
     "mxs_fused_score_batch": [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_vp],
     "mxs_fused_score_int8": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "mxs_rowsum": [c_vp, c_i64, c_i64, c_vp, c_vp],
+    "mxs_fused_score_varlen": [c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int,
+                               c_vp],
+    "mxs_quantize_per_token": [c_int, c_vp, c_i64, c_i64, c_int, c_vp, c_vp, c_vp],
+    "mxs_csr_workspace_bytes": [c_i64, c_i64],
+    "mxs_build_inverse_csr": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
+    "mxs_grad_docs_csr": [c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "mxs_grad_query": [c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "mxs_topk_workspace_bytes": [c_i64, c_i64],
+    "mxs_topk": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
+    "mxs_topk_candidates": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
 }
 _RESTYPES = {
     "mxs_version": ctypes.c_char_p,
     "mxs_status_string": ctypes.c_char_p,
     "mxs_last_error": ctypes.c_char_p,
+    "mxs_csr_workspace_bytes": ctypes.c_size_t,
+    "mxs_topk_workspace_bytes": ctypes.c_size_t,
 }
 
 MXS_F32, MXS_F16, MXS_BF16, MXS_I8 = 0, 1, 2, 3

@@ -1,0 +1,106 @@
+"""torch.autograd integration: MaxSim as a differentiable op whose backward is the paper's
+inverse-grid CSR construction ("inside autograd"; the reference has no autograd,
+SPEC.md:305).
+
+forward  : tcgen05 fused scoring, saves only the int32 argmax (N_q x B x L_q)
+backward : dQ by the gather kernel (K8); dD by device CSR (K6) + destination-owned
+           reduction (K7).  No [B, L_q, L_d] tensor exists in either direction.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _dev, _lib
+from .backward import csr_tensors
+
+
+def _grad_docs(Q, argmax, g, dest_off, dest_len, n_dest, max_len, dim):
+    row_ptr, col_idx, _ = csr_tensors(argmax, dest_off, dest_len, n_dest, max_len)
+    n_q, b, l_q = argmax.shape
+    dD = torch.empty((n_dest, dim), dtype=torch.float32, device=Q.device)
+    _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(row_ptr), _dev.ptr(col_idx), n_dest, _dev.ptr(g),
+              _dev.ptr(Q), n_q, b, l_q, dim, _dev.ptr(dD), _dev.stream_handle())
+    return dD
+
+
+def _grad_query(rows, doc_row_off, argmax, g, dim):
+    n_q, b, l_q = argmax.shape
+    dQ = torch.empty((n_q, l_q, dim), dtype=torch.float32, device=rows.device)
+    _lib.call("mxs_grad_query", _dev.dtype_code(rows), _dev.ptr(argmax), _dev.ptr(g), _dev.ptr(rows),
+              _dev.ptr(doc_row_off), n_q, b, l_q, dim, _dev.ptr(dQ), _dev.stream_handle())
+    return dQ
+
+
+class MaxSimFunction(torch.autograd.Function):
+    """scores[q, b] = sum_i max_{j < valid_len[b]} <Q[q, i], D[b, j]>  (float64 output)."""
+
+    @staticmethod
+    def forward(ctx, Q, D, valid_lens=None, exact=None):
+        from .forward import score_dense
+
+        scores, argmax, _ = score_dense(Q.detach(), D.detach(), valid_lens, exact=exact)
+        ctx.save_for_backward(Q, D, argmax)
+        ctx.mark_non_differentiable(argmax)
+        return scores, argmax
+
+    @staticmethod
+    def backward(ctx, grad_scores, _grad_argmax=None):
+        Q, D, argmax = ctx.saved_tensors
+        g = grad_scores.to(torch.float32).contiguous()
+        b, l_pad, dim = D.shape
+        Qc = Q.detach().to(D.dtype).contiguous()
+        Dc = D.detach().contiguous()
+        dQ = dD = None
+        if ctx.needs_input_grad[0]:
+            off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
+            dQ = _grad_query(Dc.reshape(b * l_pad, dim), off, argmax, g, dim).to(Q.dtype)
+        if ctx.needs_input_grad[1]:
+            off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
+            lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
+            dD = _grad_docs(Qc, argmax, g, off, lens, b * l_pad, l_pad, dim).reshape(b, l_pad, dim).to(D.dtype)
+        return dQ, dD, None, None
+
+
+class MaxSimVarlenFunction(torch.autograd.Function):
+    """Packed-corpus variant: tokens [T, d] delimited by cu_seqlens (int64 [B + 1], CUDA)."""
+
+    @staticmethod
+    def forward(ctx, Q, tokens, cu_dev, max_doc_len, exact=None):
+        from .varlen import score_varlen
+
+        scores, argmax, _ = score_varlen(Q.detach(), tokens.detach(), cu_dev, exact=exact)
+        ctx.save_for_backward(Q, tokens, cu_dev, argmax)
+        ctx.max_doc_len = int(max_doc_len)
+        ctx.mark_non_differentiable(argmax)
+        return scores, argmax
+
+    @staticmethod
+    def backward(ctx, grad_scores, _grad_argmax=None):
+        Q, tokens, cu, argmax = ctx.saved_tensors
+        g = grad_scores.to(torch.float32).contiguous()
+        dim = tokens.shape[1]
+        off = cu[:-1].contiguous()
+        dQ = dT = None
+        if ctx.needs_input_grad[0]:
+            dQ = _grad_query(tokens.detach().contiguous(), off, argmax, g, dim).to(Q.dtype)
+        if ctx.needs_input_grad[1]:
+            lens = (cu[1:] - cu[:-1]).contiguous()
+            Qc = Q.detach().to(tokens.dtype).contiguous()
+            dT = _grad_docs(Qc, argmax, g, off, lens, tokens.shape[0], ctx.max_doc_len, dim).to(tokens.dtype)
+        return dQ, dT, None, None, None
+
+
+def maxsim(Q: torch.Tensor, D: torch.Tensor, valid_lens: torch.Tensor | None = None, exact=None):
+    """Differentiable MaxSim: Q [N_q, L_q, d], D [B, L, d] -> scores f64 [N_q, B]."""
+    scores, _ = MaxSimFunction.apply(Q, D, valid_lens, exact)
+    return scores
+
+
+def maxsim_varlen(Q: torch.Tensor, tokens: torch.Tensor, cu_seqlens, exact=None):
+    """Differentiable packed MaxSim: Q [N_q, L_q, d], tokens [T, d], cu_seqlens [B + 1]."""
+    cu = cu_seqlens if isinstance(cu_seqlens, torch.Tensor) else torch.as_tensor(cu_seqlens)
+    max_len = int((cu[1:] - cu[:-1]).max().item())
+    cu = cu.to(device=tokens.device, dtype=torch.int64).contiguous()
+    scores, _ = MaxSimVarlenFunction.apply(Q, tokens, cu, max_len, exact)
+    return scores

@@ -9,6 +9,10 @@
 #include "../../include/maxsim_b200.h"
 #include "fwd_exact.cuh"
 #include "fwd_tc.cuh"
+#include "csr.cuh"
+#include "grad.cuh"
+#include "quant.cuh"
+#include "topk.cuh"
 
 namespace {
 
@@ -242,6 +246,192 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
                                          argmax, st);
   if (s != MXS_OK) return s;
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
+}
+
+
+int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, int levels, int8_t* q, float* scale,
+                           void* stream) {
+  if (!x || !q || !scale) return fail(MXS_INVALID_ARGUMENT, "mxs_quantize_per_token: null pointer");
+  if (rows < 0 || dim < 1) return fail(MXS_SHAPE_MISMATCH, "mxs_quantize_per_token: bad shape");
+  if (levels < 1 || levels > 127) return fail(MXS_INVALID_ARGUMENT, "levels must be in [1, 127], got %d", levels);
+  if (rows == 0) return MXS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long blocks = (rows * 32 + 255) / 256;
+  if (dtype == MXS_F32)
+    mxs::quantize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, rows, (int)dim, levels, q, scale);
+  else if (dtype == MXS_BF16)
+    mxs::quantize_kernel<__nv_bfloat16>
+        <<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, rows, (int)dim, levels, q, scale);
+  else if (dtype == MXS_F16)
+    mxs::quantize_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)x, rows, (int)dim, levels, q, scale);
+  else
+    return fail(MXS_UNSUPPORTED, "mxs_quantize_per_token: dtype %d", dtype);
+  return check_launch("quantize_kernel");
+}
+
+size_t mxs_csr_workspace_bytes(int64_t n_q, int64_t n_dest) { return (size_t)(n_q * n_dest) * sizeof(int32_t); }
+
+int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, int64_t l_q, const int64_t* dest_off,
+                          const int64_t* dest_len, int64_t n_dest, int64_t max_dest_len, int32_t* row_ptr,
+                          int32_t* col_idx, void* ws, size_t ws_bytes, void* stream) {
+  if (!argmax || !dest_off || !dest_len || !row_ptr || !col_idx || !ws)
+    return fail(MXS_INVALID_ARGUMENT, "mxs_build_inverse_csr: null pointer");
+  if (n_q < 1 || n_docs < 1 || l_q < 1 || n_dest < 1) return fail(MXS_SHAPE_MISMATCH, "mxs_build_inverse_csr: bad shape");
+  if (n_q * n_docs * l_q >= (1LL << 31) || n_dest >= (1LL << 31))
+    return fail(MXS_UNSUPPORTED, "mxs_build_inverse_csr: more than 2^31 sources or destinations");
+  if (ws_bytes < mxs_csr_workspace_bytes(n_q, n_dest))
+    return fail(MXS_INVALID_ARGUMENT, "mxs_build_inverse_csr: workspace too small");
+  const size_t hist_bytes = (size_t)max_dest_len * sizeof(int32_t);
+  if (hist_bytes > 200 * 1024) return fail(MXS_UNSUPPORTED, "document longer than %lld rows", (long long)(200 * 256));
+  mxs::CsrParams p;
+  p.argmax = argmax;
+  p.dest_off = (const long long*)dest_off;
+  p.dest_len = (const long long*)dest_len;
+  p.n_q = (int)n_q;
+  p.n_docs = (int)n_docs;
+  p.l_q = (int)l_q;
+  p.n_dest = n_dest;
+  p.cnt = (int32_t*)ws;
+  p.row_ptr = row_ptr;
+  p.col_idx = col_idx;
+  cudaStream_t st = (cudaStream_t)stream;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(mxs::csr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mxs::csr_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  const unsigned segs = (unsigned)(n_q * n_docs);
+  // rows that belong to no document (never the case for padded / packed layouts) stay zero
+  if (cudaMemsetAsync(ws, 0, mxs_csr_workspace_bytes(n_q, n_dest), st) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "memset");
+  if (cudaMemsetAsync(row_ptr, 0, sizeof(int32_t) * (size_t)(n_dest + 1), st) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "memset");
+  mxs::csr_count_kernel<<<segs, 256, hist_bytes, st>>>(p);
+  int s;
+  if ((s = check_launch("csr_count_kernel")) != MXS_OK) return s;
+  mxs::csr_scan_kernel<<<(unsigned)n_docs, 1024, 0, st>>>(p);
+  if ((s = check_launch("csr_scan_kernel")) != MXS_OK) return s;
+  mxs::csr_place_kernel<<<segs, 256, hist_bytes, st>>>(p);
+  return check_launch("csr_place_kernel");
+}
+
+int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx, int64_t n_dest, const float* g,
+                      const void* Q, int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, float* dD, void* stream) {
+  if (!row_ptr || !col_idx || !g || !Q || !dD) return fail(MXS_INVALID_ARGUMENT, "mxs_grad_docs_csr: null pointer");
+  if (dim < 1 || dim > 512) return fail(MXS_UNSUPPORTED, "mxs_grad_docs_csr: dim %lld outside [1, 512]", (long long)dim);
+  if (n_dest < 1) return MXS_OK;
+  mxs::GradParams p = {};
+  p.n_q = (int)n_q;
+  p.n_docs = (int)n_docs;
+  p.l_q = (int)l_q;
+  p.dim = (int)dim;
+  p.g = g;
+  p.row_ptr = row_ptr;
+  p.col_idx = col_idx;
+  p.n_dest = n_dest;
+  p.dD = dD;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long blocks = (n_dest * 32 + 255) / 256;
+  if (dtype == MXS_F32)
+    mxs::grad_docs_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)Q, p);
+  else if (dtype == MXS_BF16)
+    mxs::grad_docs_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)Q, p);
+  else if (dtype == MXS_F16)
+    mxs::grad_docs_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)Q, p);
+  else
+    return fail(MXS_UNSUPPORTED, "mxs_grad_docs_csr: dtype %d", dtype);
+  return check_launch("grad_docs_kernel");
+}
+
+int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void* D, const int64_t* doc_row_off,
+                   int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, float* dQ, void* stream) {
+  if (!argmax || !g || !D || !doc_row_off || !dQ) return fail(MXS_INVALID_ARGUMENT, "mxs_grad_query: null pointer");
+  if (dim < 1 || dim > 512) return fail(MXS_UNSUPPORTED, "mxs_grad_query: dim %lld outside [1, 512]", (long long)dim);
+  mxs::GradParams p = {};
+  p.n_q = (int)n_q;
+  p.n_docs = (int)n_docs;
+  p.l_q = (int)l_q;
+  p.dim = (int)dim;
+  p.g = g;
+  p.argmax = argmax;
+  p.doc_row_off = (const long long*)doc_row_off;
+  p.dQ = dQ;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long blocks = (n_q * l_q * 32 + 255) / 256;
+  if (blocks == 0) return MXS_OK;
+  if (dtype == MXS_F32)
+    mxs::grad_query_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)D, p);
+  else if (dtype == MXS_BF16)
+    mxs::grad_query_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)D, p);
+  else if (dtype == MXS_F16)
+    mxs::grad_query_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)D, p);
+  else
+    return fail(MXS_UNSUPPORTED, "mxs_grad_query: dtype %d", dtype);
+  return check_launch("grad_query_kernel");
+}
+
+static const long long kTopkChunk = 8192;
+
+size_t mxs_topk_workspace_bytes(int64_t n, int64_t k) {
+  const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+  return (size_t)(blocks * k) * (sizeof(double) + sizeof(long long));
+}
+
+int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, double* top_s, int64_t* top_id, void* ws,
+             size_t ws_bytes, void* stream) {
+  if (!scores || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk: null pointer");
+  if (k > n) return fail(MXS_K_TOO_LARGE, "top-%lld requested from a corpus of %lld documents", (long long)k, (long long)n);
+  if (k <= 0) return MXS_OK;
+  if (k > 4096) return fail(MXS_UNSUPPORTED, "mxs_topk: k > 4096");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+  if (blocks == 1) {
+    mxs::topk_kernel<<<1, 512, 0, st>>>(scores, nullptr, n, (int)k, n, id_offset, top_s, (long long*)top_id);
+    return check_launch("topk_kernel");
+  }
+  if (!ws || ws_bytes < mxs_topk_workspace_bytes(n, k)) return fail(MXS_INVALID_ARGUMENT, "mxs_topk: workspace too small");
+  double* cs = (double*)ws;
+  long long* ci = (long long*)(cs + blocks * k);
+  mxs::topk_kernel<<<(unsigned)blocks, 512, 0, st>>>(scores, nullptr, n, (int)k, kTopkChunk, id_offset, cs, ci);
+  int s;
+  if ((s = check_launch("topk_kernel")) != MXS_OK) return s;
+  mxs::topk_kernel<<<1, 512, 0, st>>>(cs, ci, blocks * k, (int)k, blocks * k, 0, top_s, (long long*)top_id);
+  return check_launch("topk_kernel");
+}
+
+
+int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* tokens,
+                           const int64_t* cu_seqlens, int64_t n_docs, int64_t n_tokens, int64_t dim, double* scores,
+                           int32_t* argmax, float* rowmax, int exact, void* stream) {
+  if (!Q || !tokens || !cu_seqlens || !scores || !rowmax)
+    return fail(MXS_INVALID_ARGUMENT, "mxs_fused_score_varlen: null pointer");
+  if (n_q < 1 || n_docs < 1 || l_q < 1 || dim < 1 || n_tokens < 1)
+    return fail(MXS_SHAPE_MISMATCH, "mxs_fused_score_varlen: non-positive shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  int s;
+  (void)exact;
+  const long long* cu = (const long long*)cu_seqlens;
+  if (dtype == MXS_F32)
+    s = launch_fwd_exact<float>(Q, n_q, l_q, tokens, n_docs, 0, dim, nullptr, cu, rowmax, argmax, st);
+  else if (dtype == MXS_BF16)
+    s = launch_fwd_exact<__nv_bfloat16>(Q, n_q, l_q, tokens, n_docs, 0, dim, nullptr, cu, rowmax, argmax, st);
+  else if (dtype == MXS_F16)
+    s = launch_fwd_exact<__half>(Q, n_q, l_q, tokens, n_docs, 0, dim, nullptr, cu, rowmax, argmax, st);
+  else
+    return fail(MXS_UNSUPPORTED, "mxs_fused_score_varlen: dtype %d", dtype);
+  if (s != MXS_OK) return s;
+  return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
+}
+
+
+int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
+                        void* stream) {
+  if (!scores || !ids || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk_candidates: null pointer");
+  if (k <= 0) return MXS_OK;
+  if (k > 4096) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: k > 4096");
+  mxs::topk_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(scores, (const long long*)ids, n, (int)k, n, 0, top_s,
+                                                        (long long*)top_id);
+  return check_launch("topk_kernel");
 }
 
 }  // extern "C"

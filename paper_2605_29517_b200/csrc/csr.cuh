@@ -1,0 +1,131 @@
+// Inverse-grid CSR of the saved argmax (K6), on device, bit-identical to
+// maxsim/backward.py:81-109 (bincount -> cumsum -> STABLE argsort of the flat destinations).
+//
+// Source s = (q * B + b) * L_q + i picks destination row dest_off[b] + argmax[s].  Every source
+// of document b lands in b's rows, so b's bucket block starts at row_ptr = b * N_q * L_q and the
+// problem splits per document.  Stability (ascending s inside each bucket) is ascending (q, i)
+// within the document, obtained in three passes without global atomics:
+//   1. csr_count_kernel   block (q, b): smem histogram of argmax[q, b, :] -> cnt[q][dest row]
+//   2. csr_scan_kernel    block b: totals over q, exclusive scan over b's rows -> row_ptr;
+//                         cnt[q][r] becomes the first slot of segment (q, b) inside bucket r
+//   3. csr_place_kernel   block (q, b): stable in-segment ranks (warp match + warp-ordered
+//                         cursor updates) -> col_idx[slot] = s
+// Indices are int32 (n_src and n_dest < 2^31 are checked on the host).
+#pragma once
+#include "ptx.cuh"
+
+namespace mxs {
+
+struct CsrParams {
+  const int32_t* argmax;    // [n_q, B, l_q]
+  const long long* dest_off;  // [B] first destination row of each document
+  const long long* dest_len;  // [B] destination rows owned by each document
+  int n_q, n_docs, l_q;
+  long long n_dest;
+  int32_t* cnt;             // workspace [n_q][n_dest]
+  int32_t* row_ptr;         // [n_dest + 1]
+  int32_t* col_idx;         // [n_q * B * l_q]
+};
+
+__global__ void __launch_bounds__(256) csr_count_kernel(const CsrParams p) {
+  extern __shared__ int32_t hist[];
+  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  for (int t = threadIdx.x; t < len; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  const int32_t* a = p.argmax + ((long long)q * p.n_docs + b) * p.l_q;
+  for (int i = threadIdx.x; i < p.l_q; i += blockDim.x) {
+    const int t = a[i];
+    if (t >= 0 && t < len) atomicAdd(&hist[t], 1);
+  }
+  __syncthreads();
+  int32_t* out = p.cnt + (long long)q * p.n_dest + off;
+  for (int t = threadIdx.x; t < len; t += blockDim.x) out[t] = hist[t];
+}
+
+// One block per document: rows [off, off + len).  Padding rows between documents (padded
+// layout) belong to the document before them and simply have zero count.
+__global__ void __launch_bounds__(1024) csr_scan_kernel(const CsrParams p) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  const int b = blockIdx.x;
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = (int32_t)((long long)b * p.n_q * p.l_q);
+  __syncthreads();
+  for (int t0 = 0; t0 < len; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    int tot = 0;
+    if (t < len)
+      for (int q = 0; q < p.n_q; ++q) tot += p.cnt[(long long)q * p.n_dest + off + t];
+    // block exclusive scan of tot
+    int x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int v = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      warp_tot[lane] = v;  // inclusive
+    }
+    __syncthreads();
+    const int excl = carry + (w ? warp_tot[w - 1] : 0) + x - tot;
+    if (t < len) {
+      p.row_ptr[off + t] = excl;
+      int run = excl;
+      for (int q = 0; q < p.n_q; ++q) {
+        int32_t* c = p.cnt + (long long)q * p.n_dest + off + t;
+        const int v = *c;
+        *c = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + tot;
+    __syncthreads();
+  }
+  if (b == p.n_docs - 1 && threadIdx.x == 0) p.row_ptr[p.n_dest] = (int32_t)((long long)p.n_docs * p.n_q * p.l_q);
+}
+
+// One block per (q, b) segment; warps take turns in source order so that the per-bucket
+// cursor advances exactly as a sequential stable scatter would.
+__global__ void __launch_bounds__(256) csr_place_kernel(const CsrParams p) {
+  extern __shared__ int32_t cursor[];
+  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;
+  for (int t = threadIdx.x; t < len; t += blockDim.x) cursor[t] = base[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const long long src0 = ((long long)q * p.n_docs + b) * p.l_q;
+  const int32_t* a = p.argmax + src0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int i0 = 0; i0 < p.l_q; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool valid = i < p.l_q;
+    const int key = valid ? a[i] : -1 - lane;  // distinct dummy keys never match real ones
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int rank = __popc(peers & lt_mask);
+    for (int ww = 0; ww < nw; ++ww) {
+      if (w == ww && valid) {
+        p.col_idx[cursor[key] + rank] = (int32_t)(src0 + i);
+      }
+      __syncwarp();
+      if (w == ww && valid && rank == 0) cursor[key] += __popc(peers);
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace mxs

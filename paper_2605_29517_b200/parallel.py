@@ -1,0 +1,111 @@
+"""Corpus / in-batch sharding across the GPUs of one node.
+
+One process per GPU over torch.distributed.  The data path has no collective: each rank
+scores its own contiguous document shard.  NCCL carries exactly three things:
+  * rerank  : all_gather of each rank's K (score, global id) candidates -> identical global
+              top-K (score desc, id asc) on every rank (k * 16 B per rank);
+  * training: all_gather of the [N_q, B/W] local score blocks for the in-batch loss, and the
+              all_reduce(sum) of the dQ partials (Q is replicated, dD stays shard-local).
+Shards are balanced by token count (`shard_bounds`), so the varlen corpus splits evenly.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .topk import merge_topk_across_ranks, topk
+
+
+def shard_bounds(n_docs: int, world: int, rank: int, weights=None):
+    """Contiguous [lo, hi) document range of `rank`, balanced by `weights` (doc lengths) if given."""
+    if weights is None:
+        lo = (n_docs * rank) // world
+        hi = (n_docs * (rank + 1)) // world
+        return lo, hi
+    w = np.asarray(weights, dtype=np.int64)
+    cum = np.concatenate([[0], np.cumsum(w)])
+    total = cum[-1]
+    lo = int(np.searchsorted(cum, total * rank / world, side="left"))
+    hi = int(np.searchsorted(cum, total * (rank + 1) / world, side="left")) if rank + 1 < world else n_docs
+    return min(lo, n_docs), min(hi, n_docs)
+
+
+def sharded_topk(local_scores: torch.Tensor, k: int, doc_offset: int, group=None):
+    """Global top-K of a doc-sharded score vector: device top-K per rank, then one all_gather."""
+    kk = min(k, local_scores.numel())
+    ts, ti = topk(local_scores, kk, id_offset=doc_offset)
+    if kk < k:  # pad so every rank contributes k slots
+        pad = k - kk
+        ts = torch.cat([ts, torch.full((pad,), float("-inf"), dtype=ts.dtype, device=ts.device)])
+        ti = torch.cat([ti, torch.full((pad,), -1, dtype=ti.dtype, device=ti.device)])
+    return merge_topk_across_ranks(ts, ti, k, group=group)
+
+
+def softmax_ce(scores: torch.Tensor):
+    """In-batch contrastive loss with positives on the diagonal (maxsim/cli.py:198-206), float64."""
+    s = scores.to(torch.float64)
+    b = s.shape[0]
+    mx = s.max(dim=1, keepdim=True).values
+    lse = torch.log(torch.exp(s - mx).sum(dim=1)) + mx[:, 0]
+    loss = torch.mean(lse - torch.diagonal(s))
+    probs = torch.exp(s - lse[:, None])
+    grad = (probs - torch.eye(b, dtype=s.dtype, device=s.device)) / b
+    return loss, grad
+
+
+class DeviceKernels:
+    """The sm_100a kernels used by inbatch_step (tests substitute an oracle-backed twin)."""
+
+    @staticmethod
+    def score(Q, D, valid_lens):
+        from .forward import score_dense
+
+        scores, argmax, _ = score_dense(Q, D, valid_lens)
+        return scores, argmax
+
+    @staticmethod
+    def grad_docs(Q, argmax, g, l_pad):
+        from .autograd import _grad_docs
+
+        b_local = argmax.shape[1]
+        off = torch.arange(b_local, dtype=torch.int64, device=Q.device) * l_pad
+        lens = torch.full((b_local,), l_pad, dtype=torch.int64, device=Q.device)
+        return _grad_docs(Q, argmax, g, off, lens, b_local * l_pad, l_pad, Q.shape[-1])
+
+    @staticmethod
+    def grad_query(D, argmax, g):
+        from .autograd import _grad_query
+
+        b_local, l_pad, dim = D.shape
+        off = torch.arange(b_local, dtype=torch.int64, device=D.device) * l_pad
+        return _grad_query(D.reshape(b_local * l_pad, dim).contiguous(), off, argmax, g, dim)
+
+
+def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=None, valid_lens=None,
+                 kernels=DeviceKernels):
+    """One in-batch-negatives training step with B sharded over ranks (C3 at N GPUs).
+
+    Q [N_q, L_q, d] replicated; D_local [B/W, L, d] this rank's documents starting at global
+    doc `doc_offset`.  Returns (loss, scores [N_q, B], dQ [N_q, L_q, d] fp32 all-reduced,
+    dD_local [B/W, L, d] fp32).  Collectives: one all_gather of the local score blocks, one
+    all_reduce(sum) of dQ; dD never leaves its rank.
+    """
+    import torch.distributed as dist
+
+    scores_local, argmax = kernels.score(Q, D_local, valid_lens)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world > 1:
+        parts = [torch.empty_like(scores_local) for _ in range(world)]
+        dist.all_gather(parts, scores_local.contiguous(), group=group)
+        scores = torch.cat(parts, dim=1)
+    else:
+        scores = scores_local
+    loss, g_full = softmax_ce(scores)
+    b_local, l_pad, dim = D_local.shape
+    g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
+    dD = kernels.grad_docs(Q.to(D_local.dtype).contiguous(), argmax, g, l_pad)
+    dQ = kernels.grad_query(D_local, argmax, g)
+    if world > 1:
+        dist.all_reduce(dQ, group=group)
+    return loss, scores, dQ, dD.reshape(b_local, l_pad, dim)
