@@ -1,0 +1,486 @@
+#!/usr/bin/env python
+"""Headline benchmark: BASELINE.json metric "MaxSim docs/sec at ColPali 1024x1024x128 (10K docs);
+% of tensor-core peak" on configs[1] (ColPali rerank, 1 query vs 10K docs, L_q = L_d = 1024,
+d = 128, bf16), one process per GPU.
+
+A step = score one GPU's 10K-document shard with the fused tcgen05 kernel (per-row max +
+argmax + f64 score) and select the top-20 on the device; for N > 1 the per-rank top-20 lists
+are merged with one NCCL all_gather.  Weak scaling: every rank owns its own 10K docs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own CPU path
+(baseline/_ref `maxsim`, else the oracle port) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MaxSim docs/sec at ColPali 1024×1024×128 (10K docs); % of tensor-core peak"
+UNIT = "docs/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--docs", type=int, default=10000)
+    ap.add_argument("--lq", type=int, default=1024)
+    ap.add_argument("--ld", type=int, default=1024)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--topk", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except OSError:
+        return dict(PEAKS_FALLBACK), "fallback"
+
+
+def workload_config(a, world):
+    return {
+        "workload": f"configs[1] ColPali rerank: 1 query x {a.docs} docs per GPU, L_q={a.lq}, L_d={a.ld}, d={a.dim}, "
+                    f"bf16, top-{a.topk}",
+        "n_docs_per_gpu": a.docs,
+        "n_docs_total": a.docs * world,
+        "l_q": a.lq,
+        "l_d": a.ld,
+        "dim": a.dim,
+        "topk": a.topk,
+        "inputs": "synthetic unit-norm Gaussian token embeddings (maxsim/synth.py:15-20 recipe), seeded per rank",
+        "l2": f"inputs {a.docs * a.ld * a.dim * 2 / 1e9:.2f} GB per GPU exceed the 126 MB L2 (no flush needed)",
+        "parallelism": f"dp{world}: doc-sharded, per-rank device top-{a.topk}, NCCL all_gather merge",
+    }
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s, p in zip(sm, power) if p > 300] or sm
+        return {
+            "sm_mhz": statistics.median(loaded) if loaded else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+            "power_w_max": max(power) if power else None,
+        }
+
+
+# --------------------------------------------------------------------------- reference CPU path
+def _ref_worker_init():
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+
+
+def _ref_score_docs(args):
+    """Score `n` synthetic docs with the reference's own fused_score_batch (or the oracle port)."""
+    seed, n, lq, ld, dim, kind = args
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(seed)
+    q = orc.bf16_round(orc.unit_tokens(rng, lq, dim))
+    docs = orc.bf16_round(np.stack([orc.unit_tokens(rng, ld, dim) for _ in range(n)]))
+    t0 = time.perf_counter()
+    if kind == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+        import maxsim
+
+        scores, _, _ = maxsim.fused_score_batch([maxsim.EmbeddingMatrix(q)], maxsim.DocBatch.from_dense(docs))
+        vals = scores.values
+    else:
+        vals, _ = orc.fused_score_batch(q[None], docs)
+    return time.perf_counter() - t0, float(vals.sum())
+
+
+def reference_kind():
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+        import maxsim  # noqa: F401
+
+        return "reference"
+    except ImportError:
+        return "port"
+
+
+class CpuPool:
+    def __init__(self, cores: int):
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        self.cores = cores
+        self.pool = ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"),
+                                        initializer=_ref_worker_init)
+
+    def run(self, per_worker, lq, ld, dim, kind, seed0=0):
+        jobs = [(seed0 + i, per_worker, lq, ld, dim, kind) for i in range(self.cores)]
+        t0 = time.perf_counter()
+        list(self.pool.map(_ref_score_docs, jobs))
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(a, per_worker=8):
+    kind = reference_kind()
+    cores = cpu_cores()
+    pool = CpuPool(cores)
+    pool.run(1, 8, 8, a.dim, kind)  # spawn + import warm-up, untimed
+    wall = pool.run(per_worker, a.lq, a.ld, a.dim, kind, seed0=100)
+    pool.close()
+    docs = per_worker * cores
+    return {
+        "value": docs / wall,
+        "unit": UNIT,
+        "cores": cores,
+        "kind": kind,
+        "sample": f"{docs} docs ({per_worker}/core) of the same shape ({a.lq}x{a.ld}x{a.dim}, bf16-rounded values "
+                  f"widened to fp32), {'baseline/_ref maxsim.fused_score_batch' if kind == 'reference' else 'oracle C port'}"
+                  f", ProcessPool x{cores}, {wall:.1f} s wall",
+    }
+
+
+def run_reference_arm(a, rank, world):
+    if rank != 0:
+        return
+    kind = reference_kind()
+    cores = cpu_cores()
+    pool = CpuPool(cores)
+    pool.run(1, 8, 8, a.dim, kind)
+    per_worker = 1
+    for i in range(a.warmup):
+        pool.run(per_worker, a.lq, a.ld, a.dim, kind, seed0=1000 * (i + 1))
+    wall = 0.0
+    for i in range(a.steps):
+        wall += pool.run(per_worker, a.lq, a.ld, a.dim, kind, seed0=50000 + 1000 * i)
+    pool.close()
+    docs = per_worker * cores * a.steps
+    value = docs / wall
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": wall / a.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": workload_config(a, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"each step: {per_worker * cores} docs ({per_worker}/core) of the configs[1] shape "
+                                   f"through {'maxsim.fused_score_batch (baseline/_ref)' if kind == 'reference' else 'the oracle C port'}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def make_inputs(a, rank, torch):
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    Q = torch.randn(1, a.lq, a.dim, device="cuda", generator=g)
+    Q = (Q / Q.norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+    D = torch.empty(a.docs, a.ld, a.dim, device="cuda", dtype=torch.bfloat16)
+    for lo in range(0, a.docs, 500):
+        hi = min(a.docs, lo + 500)
+        x = torch.randn(hi - lo, a.ld, a.dim, device="cuda", generator=g)
+        D[lo:hi] = (x / x.norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+    return Q, D
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_29517_b200 import _dev, _lib
+    from paper_2605_29517_b200.topk import select_candidates
+
+    lib = _lib.load()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    Q, D = make_inputs(a, rank, torch)
+    nb, lq = a.docs, a.lq
+    scores = torch.empty(1, nb, dtype=torch.float64, device=dev)
+    argmax = torch.empty(1, nb, lq, dtype=torch.int32, device=dev)
+    rowmax = torch.empty(1, nb, lq, dtype=torch.float32, device=dev)
+    k = a.topk
+    ws_bytes = int(lib.mxs_topk_workspace_bytes(nb, k))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    top_s = torch.empty(k, dtype=torch.float64, device=dev)
+    top_i = torch.empty(k, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    sh = _dev.stream_handle(stream)
+    doc_offset = rank * nb
+    P = _dev.ptr
+    launches_per_step = 1 + 1 + (2 if nb > 8192 else 1) + (1 if world > 1 else 0)
+
+    def step(Qb, Db, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        _lib.call("mxs_fused_rowmax_batch", _lib.MXS_BF16, P(Qb), 1, lq, P(Db), nb, a.ld, a.dim, None, P(argmax),
+                  P(rowmax), 0, sh)
+        if ev is not None:
+            ev[1].record(stream)
+        _lib.call("mxs_rowsum", P(rowmax), nb, lq, P(scores), sh)
+        _lib.call("mxs_topk", P(scores), nb, k, doc_offset, P(top_s), P(top_i), P(ws), ws_bytes, sh)
+        if world > 1:
+            return select_candidates(*_gather(top_s, top_i, world, dist), k)
+        return top_s, top_i
+
+    for _ in range(a.warmup):
+        step(Q, D)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(a.steps):
+        step(Q, D, evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    elapsed_ms = t0.elapsed_time(t1)
+    fwd_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    el = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    max_ms = float(el.item())
+
+    # ---- end to end through the public API with HOST buffers (pinned), copies in the timed region
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, Q, D, rank, world, dev, torch, dist)
+
+    if rank != 0:
+        return
+    peaks, peak_src = load_peaks()
+    flops_per_launch = 2.0 * lq * a.ld * a.dim * nb
+    avg_fwd_s = statistics.mean(fwd_ms) / 1e3
+    achieved = flops_per_launch / avg_fwd_s / 1e12
+    peak = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "fwd_c2_ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    value = world * nb * a.steps / (max_ms / 1e3)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": max_ms / a.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": workload_config(a, world),
+        "pct_of_tensor_peak": 100.0 * achieved / peak,
+        "roofline": {
+            "bound": "tensor",
+            "kernel": "fwd_tc_kernel<BF16> (mxs_fused_rowmax_batch)",
+            "achieved": achieved,
+            "peak": peak,
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_src})",
+            "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "flops_per_launch": flops_per_launch,
+            "avg_launch_ms": avg_fwd_s * 1e3,
+            "share_of_step": statistics.mean(fwd_ms) / (elapsed_ms / a.steps),
+        },
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clocks,
+    }
+    if not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(a)
+    print(json.dumps(line), flush=True)
+
+
+def _gather(top_s, top_i, world, dist):
+    import torch
+
+    gs = [torch.empty_like(top_s) for _ in range(world)]
+    gi = [torch.empty_like(top_i) for _ in range(world)]
+    dist.all_gather(gs, top_s)
+    dist.all_gather(gi, top_i)
+    return torch.cat(gs), torch.cat(gi)
+
+
+def run_e2e(a, Q, D, rank, world, dev, torch, dist):
+    """Same metric through the public operator API with pinned HOST inputs; H2D of the step's
+    inputs and D2H of its result (scores + top-K) inside the timed region."""
+    import paper_2605_29517_b200 as mx
+
+    hq = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+    hd = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
+    hq.copy_(Q)
+    hd.copy_(D)
+    out_s = torch.empty((1, a.docs), dtype=torch.float64, pin_memory=True)
+    out_t = torch.empty(a.topk, dtype=torch.int64, pin_memory=True)
+    dq = torch.empty_like(Q)
+    dd = torch.empty_like(D)
+    stream = torch.cuda.current_stream()
+    steps = max(1, min(a.steps, 5))
+
+    def one():
+        dq.copy_(hq, non_blocking=True)
+        dd.copy_(hd, non_blocking=True)
+        scores, _, _ = mx.score_dense(dq, dd)
+        ts, ti = mx.topk(scores[0], a.topk, id_offset=rank * a.docs)
+        out_s.copy_(scores, non_blocking=True)
+        out_t.copy_(ti, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    del hd, dd
+    return {
+        "value": world * a.docs * steps / (float(ms.item()) / 1e3),
+        "unit": UNIT,
+        "h2d_bytes_per_step": int(Q.numel() * 2 + D.numel() * 2),
+        "d2h_bytes_per_step": int(a.docs * 8 + a.topk * 8),
+        "steps": steps,
+        "path": "paper_2605_29517_b200.score_dense + topk (public API), pinned host buffers",
+    }
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference_arm(a, rank, world)
+        return
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,14 @@ int mxs_fused_score_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, co
                           float* rowmax, int exact, void* stream);
 
 /*
+ * The fused tile kernel of mxs_fused_score_batch alone: per-row maxima (rowmax) and argmax,
+ * no f64 score fold (call mxs_rowsum for it).  Same arguments minus `scores`.
+ */
+int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
+                           int64_t l_pad, int64_t dim, const int32_t* valid_lens, int32_t* argmax, float* rowmax,
+                           int exact, void* stream);
+
+/*
  * INT8 x INT8 dense forward with fused dequantisation.  Replaces maxsim/quant.py:128
  * fused_score_int8 (batched over documents and queries; the reference is per pair).
  *   Q [n_q, l_q, dim] int8, q_scale [n_q, l_q] f32; D [n_docs, l_pad, dim] int8,

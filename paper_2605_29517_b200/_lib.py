@@ -29,6 +29,7 @@ _SIGNATURES = {
     "mxs_last_error": [],
     "mxs_device_sm_count": [],
     "mxs_fused_score_batch": [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_vp],
+    "mxs_fused_rowmax_batch": [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "mxs_fused_score_int8": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "mxs_rowsum": [c_vp, c_i64, c_i64, c_vp, c_vp],
     "mxs_fused_score_varlen": [c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int,

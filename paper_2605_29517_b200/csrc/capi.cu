@@ -172,6 +172,10 @@ int launch_fwd_exact(const void* Q, int64_t n_q, int64_t l_q, const void* D, int
 
 extern "C" {
 
+int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
+                           int64_t l_pad, int64_t dim, const int32_t* valid_lens, int32_t* argmax, float* rowmax,
+                           int exact, void* stream);
+
 const char* mxs_version(void) { return "maxsim_b200 0.1.0 (sm_100a)"; }
 
 const char* mxs_status_string(int s) {
@@ -204,7 +208,16 @@ int mxs_rowsum(const float* rowmax, int64_t n_pairs, int64_t l_q, double* scores
 int mxs_fused_score_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
                           int64_t l_pad, int64_t dim, const int32_t* valid_lens, double* scores, int32_t* argmax,
                           float* rowmax, int exact, void* stream) {
-  if (!Q || !D || !scores || !rowmax) return fail(MXS_INVALID_ARGUMENT, "mxs_fused_score_batch: null pointer");
+  if (!scores) return fail(MXS_INVALID_ARGUMENT, "mxs_fused_score_batch: null pointer");
+  int s = mxs_fused_rowmax_batch(dtype, Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, argmax, rowmax, exact, stream);
+  if (s != MXS_OK) return s;
+  return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, (cudaStream_t)stream);
+}
+
+int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
+                           int64_t l_pad, int64_t dim, const int32_t* valid_lens, int32_t* argmax, float* rowmax,
+                           int exact, void* stream) {
+  if (!Q || !D || !rowmax) return fail(MXS_INVALID_ARGUMENT, "mxs_fused_score_batch: null pointer");
   if (n_q < 1 || n_docs < 1 || l_q < 1 || l_pad < 1 || dim < 1)
     return fail(MXS_SHAPE_MISMATCH, "mxs_fused_score_batch: non-positive shape");
   if (n_q * l_q >= (1LL << 31) || n_docs * l_pad >= (1LL << 31) || n_q * n_docs * l_q >= (1LL << 40))
@@ -229,8 +242,7 @@ int mxs_fused_score_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, co
   } else {
     return fail(MXS_UNSUPPORTED, "mxs_fused_score_batch: dtype %d", dtype);
   }
-  if (s != MXS_OK) return s;
-  return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
+  return s;
 }
 
 int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int64_t l_q, const int8_t* D,

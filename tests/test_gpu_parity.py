@@ -1,0 +1,418 @@
+"""GPU parity: every sm_100a kernel, called through the operator API / C-ABI, against the oracle.
+
+Tolerances (BASELINE.json north_star):
+  * fp32 exact kernel, INT8 scores, quantisation, all argmax / CSR indices: bit-exact
+    (float argmax on the tensor-core path: rows whose oracle top-2 gap exceeds 1e-5 only);
+  * BF16 / FP16 scores: within 1e-3 relative of the FP32 oracle fed the same rounded values;
+  * gradients: within 1e-3 relative (max-norm) of the float64 oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_29517_b200 as mx
+from conftest import golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-3
+GAP = 1e-5
+
+
+def cuda(x, dtype=None):
+    t = torch.as_tensor(np.asarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def top2_gap(Q, D, valid_lens):
+    """Per-(q, b, i) gap between the best and second-best similarity (float64)."""
+    S = np.einsum("qid,bjd->qbij", Q.astype(np.float64), D.astype(np.float64))
+    L = D.shape[1]
+    mask = np.arange(L)[None, None, None, :] >= np.asarray(valid_lens)[None, :, None, None]
+    S = np.where(mask, -np.inf, S)
+    part = np.sort(S, axis=-1)
+    gap = part[..., -1] - part[..., -2] if L > 1 else np.full(part.shape[:-1], np.inf)
+    return np.where(np.isfinite(gap), gap, np.inf)
+
+
+# ------------------------------------------------------------------ exact fp32 path (K10)
+def test_exact_fp32_golden_bitwise():
+    for name in ("fwd_ragged", "fwd_ties"):
+        g = golden(name)
+        docs = mx.DocBatch.from_dense(g["D"], g["valid_lens"])
+        sc, am, rep = mx.fused_score_batch(cuda(g["Q"]), docs)
+        assert np.array_equal(sc.numpy(), g["scores"]), name
+        assert np.array_equal(am.numpy(), g["argmax"]), name
+    g = golden("fwd_hand")
+    s, a, _ = mx.fused_score_pair(g["q"], g["d"])
+    assert s == 2.5 and a.tolist() == [0, 1]
+    s, a, _ = mx.fused_score_pair(g["q"], g["d"], valid_len=1)
+    assert s == 0.5 and a.tolist() == [0, 0]
+    s, a, _ = mx.fused_score_pair(g["qn"], g["dn"], valid_len=2)
+    assert s == -0.5 and a.tolist() == [1]
+
+
+def test_exact_fp32_c1_config_bitwise_and_ledger():
+    """configs[0] (ColBERT 1x1000, 32/180/128, FP32): bit-identical to the reference."""
+    g = golden("fwd_c1")
+    Q = orc.make_queries(1, 32, 128, seed=0)
+    D, vl = orc.padded(orc.make_corpus(1000, np.full(1000, 180), 128, seed=1))
+    sc, am, rep = mx.fused_score_batch(cuda(Q), mx.DocBatch.from_dense(D, vl))
+    assert np.array_equal(sc.numpy(), g["scores"])
+    assert np.array_equal(am.numpy(), g["argmax"])
+    assert rep.mac_count == int(g["macs"]) and rep.bytes_read == int(g["bytes_read"])
+    assert rep.bytes_written == int(g["bytes_written"])
+
+
+# ------------------------------------------------------------------ tensor-core forward (K1/K2)
+@pytest.mark.parametrize(
+    "n_q,l_q,n_docs,l_pad,dim,dtype",
+    [
+        (1, 1024, 24, 1024, 128, torch.bfloat16),  # ColPali shape (C2 / C3 per-pair shape)
+        (4, 300, 40, 260, 128, torch.bfloat16),    # ragged, not tile aligned
+        (3, 32, 50, 180, 128, torch.bfloat16),     # ColBERT shape
+        (2, 200, 30, 333, 64, torch.float16),
+        (2, 520, 20, 400, 256, torch.bfloat16),
+        (1, 130, 10, 129, 96, torch.bfloat16),
+        (2, 1100, 6, 300, 128, torch.bfloat16),    # L_q > 1024: three Q row groups
+    ],
+)
+def test_tensor_core_forward_vs_oracle(n_q, l_q, n_docs, l_pad, dim, dtype):
+    rng = np.random.default_rng(n_q * 1000 + l_q)
+    Q = orc.make_queries(n_q, l_q, dim, seed=int(rng.integers(1 << 30)))
+    lens = rng.integers(1, l_pad + 1, n_docs)
+    lens[0] = l_pad
+    D, vl = orc.padded(orc.make_corpus(n_docs, lens, dim, seed=int(rng.integers(1 << 30))), l_pad)
+    Qr = cuda(Q, dtype)
+    Dr = cuda(D, dtype)
+    sc, am, _ = mx.fused_score_batch(Qr, mx.DocBatch.from_dense(Dr, vl))
+    # oracle fed the rounded values widened to fp32
+    Qo = Qr.float().cpu().numpy()
+    Do = Dr.float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_batch(Qo, Do, vl)
+    assert rel_err(sc.numpy(), ref_s) < REL
+    safe = top2_gap(Qo, Do, vl) > GAP
+    assert np.array_equal(am.numpy()[safe], ref_a[safe])
+    assert safe.mean() > 0.99
+
+
+def test_tensor_core_top20_agreement_planted():
+    """100% top-20 agreement with the fp32 oracle on a planted corpus (no boundary near-ties)."""
+    q = orc.make_queries(1, 64, 128, seed=11)[0]
+    docs = orc.planted_corpus(q, 200, 96, seed=12)
+    D, vl = orc.padded(docs)
+    sc, _, _ = mx.fused_score_batch(cuda(q[None], torch.bfloat16), mx.DocBatch.from_dense(cuda(D, torch.bfloat16), vl))
+    ref, _ = orc.fused_score_batch(q[None], D, vl)
+    top_gpu = np.lexsort((np.arange(200), -sc.numpy()[0]))[:20]
+    top_ref = np.lexsort((np.arange(200), -ref[0]))[:20]
+    assert list(top_gpu) == list(top_ref)
+
+
+def test_forward_deterministic_and_shard_invariant():
+    rng = np.random.default_rng(7)
+    Q = cuda(orc.make_queries(2, 256, 128, seed=1), torch.bfloat16)
+    D = cuda(rng.standard_normal((64, 256, 128)).astype(np.float32), torch.bfloat16)
+    s1, a1, _ = mx.score_dense(Q, D)
+    s2, a2, _ = mx.score_dense(Q, D)
+    assert torch.equal(s1, s2) and torch.equal(a1, a2)
+    # emulated corpus sharding: each shard scored alone gives the same bits
+    parts = [mx.score_dense(Q, D[lo:lo + 16]) for lo in range(0, 64, 16)]
+    assert torch.equal(torch.cat([p[0] for p in parts], dim=1), s1)
+    assert torch.equal(torch.cat([p[1] for p in parts], dim=1), a1)
+    # document permutation permutes the outputs bit-for-bit
+    perm = torch.randperm(64, device="cuda")
+    sp, ap, _ = mx.score_dense(Q, D[perm].contiguous())
+    assert torch.equal(sp, s1[:, perm]) and torch.equal(ap, a1[:, perm])
+
+
+def test_c2_scale_sampled_parity():
+    """ColPali rerank at full size (10K docs): sampled oracle check + size-independent properties."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    nb = 10000
+    Q = torch.randn(1, 1024, 128, device="cuda", generator=g)
+    Q = (Q / Q.norm(dim=-1, keepdim=True)).bfloat16()
+    D = torch.randn(nb, 1024, 128, device="cuda", generator=g, dtype=torch.bfloat16)
+    sc, am, _ = mx.score_dense(Q, D)
+    assert torch.isfinite(sc).all()
+    assert int(am.min()) >= 0 and int(am.max()) < 1024
+    idx = torch.tensor([0, 1, 4999, 7777, 9998, 9999], device="cuda")
+    Qo = Q.float().cpu().numpy()
+    Do = D.index_select(0, idx).float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_batch(Qo, Do)
+    assert rel_err(sc[:, idx].cpu().numpy(), ref_s) < REL
+    safe = top2_gap(Qo, Do, [1024] * len(idx)) > GAP
+    assert np.array_equal(am[:, idx].cpu().numpy()[safe], ref_a[safe])
+    # the two Q row groups of one document are independent: splitting the query agrees exactly
+    s_lo, a_lo, r_lo = mx.score_dense(Q[:, :512].contiguous(), D[:100])
+    _, _, r_full = mx.score_dense(Q, D[:100])
+    assert torch.equal(r_full[:, :, :512], r_lo)
+
+
+# ------------------------------------------------------------------ INT8 (K3, K4)
+def test_quantize_bitwise_against_golden():
+    g = golden("quant")
+    for x, key_q, key_s, lv in ((g["x"], "q127", "s127", 127), (g["x"], "q7", "s7", 7)):
+        qm = mx.quantize_per_token(x, levels=lv)
+        assert np.array_equal(qm.q.cpu().numpy(), g[key_q])
+        assert np.array_equal(qm.scale.cpu().numpy(), g[key_s])
+    qm = mx.quantize_per_token(np.array([[0.5, -1.0]], np.float32))
+    assert qm.q.cpu().tolist() == [[64, -127]]
+    z = mx.quantize_per_token(np.zeros((2, 3), np.float32))
+    assert np.all(z.scale.cpu().numpy() == np.float32(1e-12))
+
+
+def test_quantize_random_bitwise_vs_oracle():
+    rng = np.random.default_rng(8)
+    x = (rng.standard_normal((777, 130)) * rng.uniform(0.01, 10, (777, 1))).astype(np.float32)
+    x[5] = 0
+    q, s = orc.quantize_per_token(x)
+    qm = mx.quantize_per_token(x)
+    assert np.array_equal(qm.q.cpu().numpy(), q) and np.array_equal(qm.scale.cpu().numpy(), s)
+    xb = cuda(x, torch.bfloat16)
+    qb, sb = mx.quant.quantize_tensor(xb)
+    q2, s2 = orc.quantize_per_token(xb.float().cpu().numpy())
+    assert np.array_equal(qb.cpu().numpy(), q2) and np.array_equal(sb.cpu().numpy(), s2)
+
+
+def test_int8_golden_bitwise():
+    g = golden("int8")
+    corpus = mx.QuantizedCorpus(g["d_q"], g["d_s"])
+    sm, am, _ = mx.fused_score_int8_batch(mx.QuantizedMatrix(g["q_q"], g["q_s"]), corpus, valid_lens=g["valid_lens"])
+    assert np.array_equal(sm.numpy()[0], g["scores"])
+    assert np.array_equal(am.numpy()[0], g["argmax"])
+    s, a = mx.fused_score_int8(mx.QuantizedMatrix(g["q_q"], g["q_s"]), corpus.doc(1), valid_len=13)
+    assert s == g["scores"][1] and a.cpu().tolist() == list(g["argmax"][1])
+
+
+@pytest.mark.parametrize("l_q,n_docs,l_pad,dim", [(1024, 12, 1024, 128), (33, 40, 200, 64), (300, 9, 517, 256)])
+def test_int8_random_bitwise_incl_ties(l_q, n_docs, l_pad, dim):
+    rng = np.random.default_rng(l_q + dim)
+    Qf = rng.standard_normal((2, l_q, dim)).astype(np.float32)
+    Df = rng.standard_normal((n_docs, l_pad, dim)).astype(np.float32)
+    Df[1] = Df[0]                       # identical documents
+    Df[2, 1::2] = Df[2, 0::2][: Df[2, 1::2].shape[0]]  # duplicated rows -> exact ties
+    lens = rng.integers(1, l_pad + 1, n_docs)
+    qq, qs = mx.quant.quantize_tensor(cuda(Qf))
+    dq, ds = mx.quant.quantize_tensor(cuda(Df))
+    sc, am, _ = mx.score_int8(qq, qs, dq, ds, cuda(lens.astype(np.int32)))
+    oq, os_ = orc.quantize_per_token(Qf.reshape(-1, dim))
+    dq_o, ds_o = orc.quantize_per_token(Df.reshape(-1, dim))
+    ref_s, ref_a = orc.fused_score_int8(oq.reshape(2, l_q, dim), os_.reshape(2, l_q), dq_o.reshape(n_docs, l_pad, dim),
+                                        ds_o.reshape(n_docs, l_pad), lens)
+    assert np.array_equal(sc.cpu().numpy(), ref_s)
+    assert np.array_equal(am.cpu().numpy(), ref_a)
+
+
+def test_two_stage_topk_matches_reference():
+    g = golden("two_stage")
+    D = g["D"]
+    corpus_q = mx.quantize_corpus(cuda(D))
+    top = mx.two_stage_topk(g["q"], corpus_q, mx.DocBatch.from_dense(D), k=5)
+    assert [t[0] for t in top] == list(g["top_ids"])
+    assert [t[1] for t in top] == list(g["top_scores"])
+    with pytest.raises(mx.KTooLarge):
+        mx.two_stage_topk(g["q"], corpus_q, mx.DocBatch.from_dense(D), k=31)
+
+
+# ------------------------------------------------------------------ varlen (K5)
+def test_varlen_golden_bitwise():
+    g = golden("varlen")
+    pk = mx.PackedCorpus(g["tokens"], g["cu"])
+    s, am, rep = mx.fused_score_varlen(g["q"], pk)
+    assert np.array_equal(s.cpu().numpy(), g["scores"])
+    assert np.array_equal(am.numpy(), g["argmax"])
+    assert am.padded_len is None and rep.mac_count == int(g["macs"])
+
+
+def test_varlen_equals_padded_bf16():
+    rng = np.random.default_rng(9)
+    lens = rng.integers(32, 513, 300)
+    docs = orc.make_corpus(300, lens, 128, seed=4)
+    q = orc.make_queries(1, 32, 128, seed=5)
+    toks = cuda(np.concatenate(docs), torch.bfloat16)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    s_v, a_v, _ = mx.score_varlen(cuda(q, torch.bfloat16), toks, cuda(cu))
+    D, vl = orc.padded(docs)
+    s_p, a_p, _ = mx.score_dense(cuda(q, torch.bfloat16), cuda(D, torch.bfloat16), cuda(vl))
+    ref_s, ref_a = orc.fused_score_varlen(cuda(q, torch.bfloat16).float().cpu().numpy(), toks.float().cpu().numpy(), cu)
+    assert rel_err(s_v.cpu().numpy(), ref_s) < REL and rel_err(s_p.cpu().numpy(), ref_s) < REL
+    agree = (a_v.cpu().numpy() == ref_a).mean()
+    assert agree > 0.999
+
+
+# ------------------------------------------------------------------ backward (K6, K7, K8)
+def test_csr_bitwise_against_golden_and_oracle():
+    g = golden("csr")
+    csr = mx.build_inverse_csr(mx.ArgmaxMap(g["h_argmax"], [2], padded_len=2))
+    rp, ci = csr.to_numpy()
+    assert list(rp) == [0, 1, 3] and list(ci) == [2, 0, 1]
+    csr = mx.build_inverse_csr(mx.ArgmaxMap(np.zeros((3, 4, 5), np.int32), [6] * 4, padded_len=6))
+    rp, ci = csr.to_numpy()
+    assert np.array_equal(rp, g["hot_row_ptr"]) and np.array_equal(ci, g["hot_col_idx"])
+    csr = mx.build_inverse_csr(mx.ArgmaxMap(g["p_argmax"], g["p_lens"], padded_len=None))
+    rp, ci = csr.to_numpy()
+    assert np.array_equal(rp, g["p_row_ptr"]) and np.array_equal(ci, g["p_col_idx"])
+    assert np.array_equal(csr.destinations_per_source().cpu().numpy(),
+                          mx.ArgmaxMap(g["p_argmax"], g["p_lens"]).flat_destinations().cpu().numpy())
+
+
+def test_csr_random_maps_bitwise():
+    """tests/test_acceptance.py:192-220 style: many random maps incl. all-hot and permutations."""
+    rng = np.random.default_rng(10)
+    for trial in range(60):
+        n_q, b, l_q = rng.integers(1, 6), rng.integers(1, 7), rng.integers(1, 40)
+        L = int(rng.integers(1, 50))
+        lens = rng.integers(1, L + 1, b)
+        if trial % 3 == 0:
+            idx = np.zeros((n_q, b, l_q), np.int32)  # all hot
+        else:
+            idx = np.stack([np.stack([rng.integers(0, lens[j], l_q) for j in range(b)]) for _ in range(n_q)])
+        packed = trial % 2 == 1
+        am = mx.ArgmaxMap(idx.astype(np.int32), lens, padded_len=None if packed else L)
+        rp, ci = mx.build_inverse_csr(am).to_numpy()
+        orp, oci = orc.build_inverse_csr(idx, lens, None if packed else L)
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci), trial
+
+
+def test_csr_c3_scale_bitwise():
+    rng = np.random.default_rng(12)
+    idx = rng.integers(0, 1024, (64, 64, 1024)).astype(np.int32)
+    idx[3, 5, :] = 7  # a hot token
+    am = mx.ArgmaxMap(idx, [1024] * 64, padded_len=1024)
+    rp, ci = mx.build_inverse_csr(am).to_numpy()
+    orp, oci = orc.build_inverse_csr(idx, [1024] * 64, 1024)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+
+
+def test_backward_golden():
+    g = golden("backward")
+    docs = mx.DocBatch.from_dense(g["D"], g["valid_lens"])
+    sc, am, _ = mx.fused_score_batch(cuda(g["Q"]), docs)
+    assert np.array_equal(am.numpy(), g["argmax"])
+    dq, dd = mx.backward_dispatch(am, g["g"], cuda(g["Q"]), docs)
+    assert rel_err(dq.cpu().numpy(), g["dQ"]) < 1e-6
+    assert rel_err(dd.cpu().numpy(), g["dD"]) < 1e-6
+    flat = mx.grad_docs_csr(mx.build_inverse_csr(am), g["g"], cuda(g["Q"]))
+    assert rel_err(flat.cpu().numpy(), g["flat_dD"]) < 1e-6
+    with pytest.raises(mx.StaleCsr):
+        mx.grad_docs_csr(mx.build_inverse_csr(am), np.ones((2, 3)), cuda(np.ones((2, 9, 8), np.float32)))
+
+
+def test_inbatch_training_step_c3_shape_bf16():
+    """C3: N_q = B = 64 at ColPali shape, bf16, CSR backward, vs the float64 oracle on the same argmax."""
+    from paper_2605_29517_b200.parallel import inbatch_step
+
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    Q = torch.randn(64, 1024, 128, device="cuda", generator=gen)
+    Q = (Q / Q.norm(dim=-1, keepdim=True)).bfloat16()
+    D = torch.randn(64, 1024, 128, device="cuda", generator=gen)
+    D = (D / D.norm(dim=-1, keepdim=True)).bfloat16()
+    loss, scores, dQ, dD = inbatch_step(Q, D, 0)
+    _, am, _ = mx.score_dense(Q, D)
+    l_ref, g_ref = orc.softmax_ce(scores.cpu().numpy())
+    assert abs(float(loss) - l_ref) <= 1e-9 * abs(l_ref)
+    Qo = Q.float().cpu().numpy()
+    Do = D.float().cpu().numpy()
+    a = am.cpu().numpy()
+    dq_ref = orc.grad_query(a, g_ref, Do.reshape(-1, 128), np.arange(64) * 1024)
+    rp, ci = orc.build_inverse_csr(a, [1024] * 64, 1024)
+    dd_ref = orc.grad_docs_csr(rp, ci, g_ref, Qo, n_docs=64).reshape(64, 1024, 128)
+    assert rel_err(dQ.cpu().numpy(), dq_ref) < REL
+    assert rel_err(dD.cpu().numpy(), dd_ref) < REL
+
+
+def test_autograd_matches_oracle_and_finite_differences():
+    g = golden("inbatch")
+    Q = cuda(g["Q"]).requires_grad_(True)
+    D = cuda(g["D"]).requires_grad_(True)
+    scores = mx.maxsim(Q, D)
+    assert np.array_equal(scores.detach().cpu().numpy(), g["scores"])
+    up = cuda(g["g"])
+    (scores * up).sum().backward()
+    assert rel_err(Q.grad.cpu().numpy(), g["dQ"]) < 1e-6
+    assert rel_err(D.grad.cpu().numpy(), g["dD"]) < 1e-6
+
+
+def test_autograd_varlen_matches_padded():
+    rng = np.random.default_rng(14)
+    lens = rng.integers(3, 20, 6)
+    docs = [rng.standard_normal((int(n), 16)).astype(np.float32) for n in lens]
+    Q = cuda(rng.standard_normal((2, 5, 16)).astype(np.float32)).requires_grad_(True)
+    toks = cuda(np.concatenate(docs)).requires_grad_(True)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    up = cuda(rng.standard_normal((2, 6)))
+    (mx.maxsim_varlen(Q, toks, cu) * up).sum().backward()
+    D, vl = orc.padded(docs)
+    s, a = orc.fused_score_varlen(Q.detach().cpu().numpy(), np.concatenate(docs), cu)
+    dq_ref = orc.grad_query(a, up.cpu().numpy(), np.concatenate(docs), cu[:-1])
+    rp, ci = orc.build_inverse_csr(a, lens, None)
+    dt_ref = orc.grad_docs_csr(rp, ci, up.cpu().numpy(), Q.detach().cpu().numpy(), n_docs=6)
+    assert rel_err(Q.grad.cpu().numpy(), dq_ref) < 1e-6
+    assert rel_err(toks.grad.cpu().numpy(), dt_ref) < 1e-6
+
+
+def test_training_drift_matches_reference_loop():
+    """tests/test_acceptance.py:438-447 criterion c11 (shortened): SGD through the device path
+    tracks the float64 oracle loop; loss drift <= 1e-4."""
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((4, 6, 8)).astype(np.float32)
+    d = rng.standard_normal((4, 7, 8)).astype(np.float32)
+    qo, do = q.copy(), d.copy()
+    drift = 0.0
+    for _ in range(30):
+        Q = cuda(q).requires_grad_(True)
+        D = cuda(d).requires_grad_(True)
+        s = mx.maxsim(Q, D)
+        from paper_2605_29517_b200.parallel import softmax_ce
+
+        loss, g = softmax_ce(s.detach())
+        (s * g).sum().backward()
+        q = (q.astype(np.float64) - 0.05 * Q.grad.cpu().numpy()).astype(np.float32)
+        d = (d.astype(np.float64) - 0.05 * D.grad.cpu().numpy()).astype(np.float32)
+        so, ao = orc.fused_score_batch(qo, do)
+        lo, go = orc.softmax_ce(so)
+        dq = orc.grad_query(ao, go, do.reshape(-1, 8), np.arange(4) * 7)
+        rp, ci = orc.build_inverse_csr(ao, [7] * 4, 7)
+        dd = orc.grad_docs_csr(rp, ci, go, qo, n_docs=4).reshape(4, 7, 8)
+        qo = (qo.astype(np.float64) - 0.05 * dq).astype(np.float32)
+        do = (do.astype(np.float64) - 0.05 * dd).astype(np.float32)
+        drift = max(drift, abs(float(loss) - lo) / abs(lo))
+    assert drift <= 1e-4
+
+
+# ------------------------------------------------------------------ top-K (K9)
+def test_topk_ties_and_chunking():
+    g = golden("misc")
+    ts, ti = mx.topk(cuda(g["tie_scores"]), 15)
+    assert ti.cpu().tolist() == list(g["tie_ids"])
+    rng = np.random.default_rng(6)
+    s = np.round(rng.standard_normal(100_000), 2)  # > 8192: two-pass path, heavy ties
+    ts, ti = mx.topk(cuda(s), 20, id_offset=500)
+    os_, oi = orc.topk(s, 20, id_offset=500)
+    assert ti.cpu().tolist() == oi.tolist() and ts.cpu().tolist() == os_.tolist()
+    assert mx.ranked(cuda([0.0, 1.0, 0.5, 1.0]), 2) == [[1, 1.0], [3, 1.0]]
+    with pytest.raises(mx.KTooLarge):
+        mx.topk(cuda(s[:5]), 6)
+
+
+def test_sharded_rerank_merge_equals_global():
+    from paper_2605_29517_b200.topk import select_candidates
+
+    rng = np.random.default_rng(13)
+    s = np.round(rng.standard_normal(50_000), 2)
+    cand_s, cand_i = [], []
+    for lo in range(0, 50_000, 12_500):  # four emulated ranks
+        ts, ti = mx.topk(cuda(s[lo:lo + 12_500]), 20, id_offset=lo)
+        cand_s.append(ts)
+        cand_i.append(ti)
+    ms, mi = select_candidates(torch.cat(cand_s), torch.cat(cand_i), 20)
+    os_, oi = orc.topk(s, 20)
+    assert mi.cpu().tolist() == oi.tolist() and ms.cpu().tolist() == os_.tolist()
