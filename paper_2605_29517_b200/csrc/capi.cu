@@ -3,12 +3,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 
 #include "../../include/maxsim_b200.h"
 #include "fwd_exact.cuh"
 #include "fwd_tc.cuh"
+#include "fwd_ts.cuh"
 #include "csr.cuh"
 #include "grad.cuh"
 #include "quant.cuh"
@@ -64,12 +66,12 @@ EncodeTiledFn encode_fn() {
 
 // 2-D row-major [rows, cols] tensor, box = 128 bytes x 128 rows, SWIZZLE_128B.
 int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t cols,
-                 int64_t rows) {
+                 int64_t rows, int box_rows = 128) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(MXS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(cols * elem_bytes)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), 128u};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -134,7 +136,14 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   if ((s = make_tmap_2d(&tq, Q, dt, eb, dim, n_q * l_q)) != MXS_OK) return s;
   if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad)) != MXS_OK) return s;
   const size_t smem = mxs::fwd_tc_smem_bytes(ka, qb, stages);
-  auto kern = mxs::fwd_tc_kernel<KIND>;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::FwdTcParams) = nullptr;
+  switch (ka) {
+    case 1: kern = mxs::fwd_tc_kernel<KIND, 1>; break;
+    case 2: kern = mxs::fwd_tc_kernel<KIND, 2>; break;
+    case 3: kern = mxs::fwd_tc_kernel<KIND, 3>; break;
+    case 4: kern = mxs::fwd_tc_kernel<KIND, 4>; break;
+    default: return fail(MXS_UNSUPPORTED, "tensor-core path supports dim*elem_bytes <= 512 (dim=%lld)", (long long)dim);
+  }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
   const int nsm = sm_count();
@@ -143,6 +152,87 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   if (grid <= 0) return MXS_OK;
   kern<<<(unsigned)grid, mxs::kFwdThreads, smem, st>>>(tq, td, p);
   return check_launch("fwd_tc_kernel");
+}
+
+// v3 path: Q in TMEM, cluster multicast of document tiles, stash-based argmax.
+// Returns MXS_UNSUPPORTED (without launching) when the shape needs the SS kernel.
+template <mxs::TcKind KIND>
+int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad, int64_t dim,
+                  const int32_t* valid_lens, const float* q_scale, const float* d_scale, float* rowmax,
+                  int32_t* argmax, cudaStream_t st) {
+  const int eb = (KIND == mxs::TcKind::I8) ? 1 : 2;
+  if ((dim * eb) % 16 != 0) return MXS_UNSUPPORTED;
+  const int ka = (int)((dim * eb + 127) / 128);
+  if (ka > 4) return MXS_UNSUPPORTED;
+  const int qb_max = std::min(mxs::kMaxQb, 256 / (ka * 32));
+  const int nmb = (int)((l_q + 127) / 128);
+  const int qb = std::min(qb_max, nmb);
+  const int n_groups = (nmb + qb - 1) / qb;
+  const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
+  const size_t max_smem = 232448;
+  const size_t fixed = 1024 + sizeof(mxs::TsSmemHeader) + (size_t)qb * 128 * 128;
+  int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
+  if (stages > 8) stages = 8;
+  if (stages < 2) return MXS_UNSUPPORTED;
+  mxs::FwdTcParams p = {};
+  p.n_q = (int)n_q;
+  p.l_q = (int)l_q;
+  p.n_docs = (int)n_docs;
+  p.l_pad = (int)l_pad;
+  p.dim = (int)dim;
+  p.ka = ka;
+  p.qb = qb;
+  p.n_groups = n_groups;
+  p.stages = stages;
+  p.n_units = (cl > 1) ? (long long)n_q * n_docs : (long long)n_q * n_groups * n_docs;
+  p.valid_lens = valid_lens;
+  p.q_scale = q_scale;
+  p.d_scale = d_scale;
+  p.rowmax = rowmax;
+  p.argmax = argmax;
+  p.q_ptr = Q;
+  CUtensorMap td;
+  const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  int s;
+  if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
+  const size_t smem = mxs::fwd_ts_smem_bytes(ka, qb, stages);
+  using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
+  KernT kern = nullptr;
+#define MXS_TS_CASE(KA_, CL_) \
+  if (ka == KA_ && cl == CL_) kern = mxs::fwd_ts_kernel<KIND, KA_, CL_>;
+  MXS_TS_CASE(1, 1) MXS_TS_CASE(1, 2) MXS_TS_CASE(1, 4) MXS_TS_CASE(2, 1) MXS_TS_CASE(2, 2) MXS_TS_CASE(2, 4)
+  MXS_TS_CASE(3, 1) MXS_TS_CASE(3, 2) MXS_TS_CASE(3, 4) MXS_TS_CASE(4, 1) MXS_TS_CASE(4, 2) MXS_TS_CASE(4, 4)
+#undef MXS_TS_CASE
+  if (!kern) return MXS_UNSUPPORTED;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
+  const int nsm = sm_count();
+  if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
+  long long workers = nsm / cl;
+  if (p.n_units < workers) workers = p.n_units;
+  if (workers <= 0) return MXS_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(workers * cl));
+  cfg.blockDim = dim3(mxs::kFwdThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, td, p);
+  if (e != cudaSuccess) return fail(MXS_CUDA_ERROR, "fwd_ts_kernel launch: %s", cudaGetErrorString(e));
+  return check_launch("fwd_ts_kernel");
+}
+
+bool use_ts_path() {
+  const char* impl = getenv("MXS_FWD_IMPL");
+  return !(impl && strcmp(impl, "ss") == 0);
 }
 
 template <typename T>
@@ -234,11 +324,19 @@ int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     else
       return fail(MXS_UNSUPPORTED, "mxs_fused_score_batch: dtype %d not a float type", dtype);
   } else if (dtype == MXS_BF16) {
-    s = launch_fwd_tc<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
-                                         argmax, st);
+    s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
+                                                         nullptr, rowmax, argmax, st)
+                      : MXS_UNSUPPORTED;
+    if (s == MXS_UNSUPPORTED)
+      s = launch_fwd_tc<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
+                                           argmax, st);
   } else if (dtype == MXS_F16) {
-    s = launch_fwd_tc<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
-                                        argmax, st);
+    s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
+                                                        nullptr, rowmax, argmax, st)
+                      : MXS_UNSUPPORTED;
+    if (s == MXS_UNSUPPORTED)
+      s = launch_fwd_tc<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
+                                          argmax, st);
   } else {
     return fail(MXS_UNSUPPORTED, "mxs_fused_score_batch: dtype %d", dtype);
   }
@@ -254,8 +352,12 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
     return fail(MXS_SHAPE_MISMATCH, "mxs_fused_score_int8: non-positive shape");
   if (dim > 133000) return fail(MXS_SHAPE_MISMATCH, "dim %lld exceeds 133000 (int32 accumulation bound)", (long long)dim);
   cudaStream_t st = (cudaStream_t)stream;
-  int s = launch_fwd_tc<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale, rowmax,
-                                         argmax, st);
+  int s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale,
+                                                         d_scale, rowmax, argmax, st)
+                        : MXS_UNSUPPORTED;
+  if (s == MXS_UNSUPPORTED)
+    s = launch_fwd_tc<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale, rowmax,
+                                       argmax, st);
   if (s != MXS_OK) return s;
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
 }

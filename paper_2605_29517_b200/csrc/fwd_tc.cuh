@@ -34,6 +34,7 @@ struct FwdTcParams {
   float* rowmax;              // [n_q, n_docs, l_q]
   int32_t* argmax;            // [n_q, n_docs, l_q] or nullptr
   int debug;                  // profiling knobs (MXS_DEBUG env): 1 = skip fold, 2 = skip TMEM loads too
+  const void* q_ptr;          // Q rows in global memory (TS kernel loads them into TMEM)
 };
 
 constexpr int kTileRows = 128;     // rows per Q block and per document tile
@@ -69,28 +70,84 @@ MXS_DEV int doc_valid_len(const FwdTcParams& p, int b) {
   return p.valid_lens ? __ldg(p.valid_lens + b) : p.l_pad;
 }
 
-// Fold one 32-column chunk into the running (m, ix) of this thread's row.
-MXS_DEV void fold_chunk(float (&v)[32], int base, int vl, float& m, int& ix) {
+// max of 32 values as a 3-input tree (FMNMX3): 15 ALU instructions, depth 4.
+MXS_DEV float max32(const float (&v)[32]) {
+  float t[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) t[j] = fmax3(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
+  t[10] = fmaxf(v[30], v[31]);
+  const float a = fmax3(t[0], t[1], t[2]);
+  const float b = fmax3(t[3], t[4], t[5]);
+  const float c = fmax3(t[6], t[7], t[8]);
+  return fmax3(fmax3(a, b, c), t[9], t[10]);
+}
+
+// Lowest j with v[j] == c, assuming c = max(v) and 2^-60 <= |c| <= 2^27.
+// d_j = c - v_j >= 0 is exactly 0 iff v_j == c; otherwise d_j >= 2^-84, so
+// w_j = d_j * 2^100 + j is j for the winners and >= 2^16 for everyone else.  Two FMA-pipe
+// instructions per element and a min tree, all independent (no serial select chain).
+MXS_DEV int first_argmax32_fast(const float (&v)[32], float c) {
+  float w[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = __fmaf_rn(__fsub_rn(c, v[j]), 0x1p100f, (float)j);
+  float t[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) t[j] = fmin3(w[3 * j], w[3 * j + 1], w[3 * j + 2]);
+  t[10] = fminf(w[30], w[31]);
+  const float a = fmin3(t[0], t[1], t[2]);
+  const float b = fmin3(t[3], t[4], t[5]);
+  const float d = fmin3(t[6], t[7], t[8]);
+  return (int)fmin3(fmin3(a, b, d), t[9], t[10]);
+}
+
+// Exact fallback for extreme magnitudes: equality bitmask, first set bit.
+MXS_DEV int first_argmax32_exact(const float (&v)[32], float c) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) bits |= (v[j] == c) ? (1u << j) : 0u;
+  return __ffs(bits) - 1;
+}
+
+// Fold one 32-column chunk into the running (m, ix) of this thread's row: chunk max first,
+// index search only when some lane of the warp improves (strict >, so earlier columns win ties).
+MXS_DEV int first_argmax32_chain(const float (&v)[32], float c) {
+  int jj = 31;
+#pragma unroll
+  for (int j = 30; j >= 0; --j) jj = (v[j] == c) ? j : jj;
+  return jj;
+}
+
+MXS_DEV void fold_chunk(float (&v)[32], int base, int vl, float& m, int& ix, int variant = 0) {
   if (base + 32 > vl) {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (base + j >= vl) v[j] = -INFINITY;
   }
-  float t[11];
-#pragma unroll
-  for (int j = 0; j < 10; ++j) t[j] = fmax3(v[3 * j], v[3 * j + 1], v[3 * j + 2]);
-  t[10] = fmaxf(v[30], v[31]);
-  float a = fmax3(t[0], t[1], t[2]);
-  float b = fmax3(t[3], t[4], t[5]);
-  float c = fmax3(t[6], t[7], t[8]);
-  float d = fmaxf(t[9], t[10]);
-  const float cmax = fmaxf(fmax3(a, b, c), d);
+  const float cmax = max32(v);
   const bool upd = cmax > m;
+  if (variant == 3) {  // profiling knob: max only
+    if (upd) m = cmax;
+    return;
+  }
+  if (variant == 10 || variant == 11) {
+    if (__any_sync(0xffffffffu, upd)) {
+      const int jj = variant == 10 ? first_argmax32_chain(v, cmax) : first_argmax32_exact(v, cmax);
+      if (upd) {
+        m = cmax;
+        ix = base + jj;
+      }
+    }
+    return;
+  }
   if (__any_sync(0xffffffffu, upd)) {
+    const float ac = fabsf(cmax);
+    const bool odd = upd && !(ac >= 0x1p-60f && ac <= 0x1p27f);
+    int jj;
+    if (__any_sync(0xffffffffu, odd))
+      jj = first_argmax32_exact(v, cmax);
+    else
+      jj = first_argmax32_fast(v, cmax);
     if (upd) {
-      int jj = 31;
-#pragma unroll
-      for (int j = 30; j >= 0; --j) jj = (v[j] == cmax) ? j : jj;
       m = cmax;
       ix = base + jj;
     }
@@ -101,6 +158,7 @@ MXS_DEV void fold_chunk(float (&v)[32], int base, int vl, float& m, int& ix) {
 template <TcKind KIND>
 MXS_DEV void epi_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcParams& p, int b, float sq, float& m,
                        int& ix) {
+  const int variant = p.debug >= 3 ? p.debug : 0;
   float v[32];
   if constexpr (KIND == TcKind::I8) {
     // f32(int32 acc) rounds to nearest even like numpy's int32->float32 cast; then
@@ -116,18 +174,18 @@ MXS_DEV void epi_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPar
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
   }
-  if (base < vl) fold_chunk(v, base, vl, m, ix);
+  if (base < vl) fold_chunk(v, base, vl, m, ix, variant);
 }
 
-template <TcKind KIND>
+template <TcKind KIND, int KA>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD,
                   const FwdTcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sD = smem + (size_t)p.qb * p.ka * kAtomBytes;
-  FwdSmemHeader* hdr = reinterpret_cast<FwdSmemHeader*>(sD + (size_t)p.stages * p.ka * kAtomBytes);
+  uint8_t* sD = smem + (size_t)p.qb * KA * kAtomBytes;
+  FwdSmemHeader* hdr = reinterpret_cast<FwdSmemHeader*>(sD + (size_t)p.stages * KA * kAtomBytes);
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
@@ -178,10 +236,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             qphase ^= 1;
           }
           const int qbv = min(p.qb, nmb_total - g * p.qb);
-          mbar_arrive_expect_tx(&hdr->qfull, (uint32_t)(qbv * p.ka * kAtomBytes));
+          mbar_arrive_expect_tx(&hdr->qfull, (uint32_t)(qbv * KA * kAtomBytes));
           for (int mb = 0; mb < qbv; ++mb)
-            for (int a = 0; a < p.ka; ++a)
-              tma_load_2d(&tmQ, &hdr->qfull, sQ + (size_t)(mb * p.ka + a) * kAtomBytes, a * 128 / (KIND == TcKind::I8 ? 1 : 2),
+            for (int a = 0; a < KA; ++a)
+              tma_load_2d(&tmQ, &hdr->qfull, sQ + (size_t)(mb * KA + a) * kAtomBytes, a * 128 / (KIND == TcKind::I8 ? 1 : 2),
                           q * p.l_q + (g * p.qb + mb) * kTileRows, kEvictLast);
           cur_key = key;
         }
@@ -189,9 +247,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int ntiles = (vl + kTileRows - 1) / kTileRows;
         for (int t = 0; t < ntiles; ++t) {
           mbar_wait(&hdr->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(p.ka * kAtomBytes));
-          for (int a = 0; a < p.ka; ++a)
-            tma_load_2d(&tmD, &hdr->full[stage], sD + (size_t)(stage * p.ka + a) * kAtomBytes,
+          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
+          for (int a = 0; a < KA; ++a)
+            tma_load_2d(&tmD, &hdr->full[stage], sD + (size_t)(stage * KA + a) * kAtomBytes,
                         a * 128 / (KIND == TcKind::I8 ? 1 : 2), b * p.l_pad + t * kTileRows, kEvictNormal);
           if (++stage == p.stages) {
             stage = 0;
@@ -202,54 +260,65 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int stage = 0, slot = 0;
-      uint32_t phase = 0, sphase = 0, qphase = 0;
-      long long cur_key = -1;
-      const int ksteps = p.ka * 4;  // 32-byte K slices per 128-byte atom
-      const uint32_t sQa = smem_u32(sQ), sDa = smem_u32(sD);
-      for (long long u = u_begin; u < u_end; ++u) {
-        int q, g, b;
-        decode_unit(u, p, q, g, b);
-        const long long key = (long long)q * p.n_groups + g;
-        if (key != cur_key) {
-          if (cur_key >= 0) mma_commit(&hdr->qempty);
-          mbar_wait(&hdr->qfull, qphase);
-          qphase ^= 1;
-          tc_fence_after();
-          cur_key = key;
+    // The whole warp walks the schedule (warp-uniform state, uniform registers); one elected
+    // lane issues each MMA chain.  Descriptors are a base plus compile-time K offsets, so the
+    // issue loop is a handful of uniform adds per tcgen05.mma.
+    // Q block mb belongs to epilogue set (mb & 1); that set alternates between its two slots
+    // {set, set + 2}, so every slot's phases are consumed in order by one set (no parity aliasing).
+    int stage = 0;
+    uint32_t phase = 0, qphase = 0;
+    uint32_t uses[2] = {0u, 0u};
+    long long cur_key = -1;
+    const uint64_t qdesc0 = sw128_kmajor_desc(smem_u32(sQ));
+    const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
+    for (long long u = u_begin; u < u_end; ++u) {
+      int q, g, b;
+      decode_unit(u, p, q, g, b);
+      const long long key = (long long)q * p.n_groups + g;
+      if (key != cur_key) {
+        if (cur_key >= 0) {
+          if (elect_one()) mma_commit(&hdr->qempty);
+          __syncwarp();
         }
-        const int qbv = min(p.qb, nmb_total - g * p.qb);
-        const int vl = doc_valid_len(p, b);
-        const int ntiles = (vl + kTileRows - 1) / kTileRows;
-        for (int t = 0; t < ntiles; ++t) {
-          mbar_wait(&hdr->full[stage], phase);
+        mbar_wait(&hdr->qfull, qphase);
+        qphase ^= 1;
+        tc_fence_after();
+        cur_key = key;
+      }
+      const int qbv = min(p.qb, nmb_total - g * p.qb);
+      const int vl = doc_valid_len(p, b);
+      const int ntiles = (vl + kTileRows - 1) / kTileRows;
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait(&hdr->full[stage], phase);
+        tc_fence_after();
+        const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
+        for (int mb = 0; mb < qbv; ++mb) {
+          const int set = mb & 1;
+          const int slot = set + 2 * (int)(uses[set] & 1u);
+          const uint32_t sphase = (uses[set] >> 1) & 1u;
+          ++uses[set];
+          mbar_wait(&hdr->tempty[slot], sphase ^ 1);
           tc_fence_after();
-          for (int mb = 0; mb < qbv; ++mb) {
-            mbar_wait(&hdr->tempty[slot], sphase ^ 1);
-            tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad0 = qdesc0 + (uint64_t)((mb * KA * kAtomBytes) >> 4);
             const uint32_t dcol = tmem_base + (uint32_t)(slot * 128);
-            for (int k = 0; k < ksteps; ++k) {
-              const uint32_t aoff = (uint32_t)((mb * p.ka + (k >> 2)) * kAtomBytes + (k & 3) * 32);
-              const uint32_t boff = (uint32_t)((stage * p.ka + (k >> 2)) * kAtomBytes + (k & 3) * 32);
-              const uint64_t ad = sw128_kmajor_desc(sQa + aoff);
-              const uint64_t bd = sw128_kmajor_desc(sDa + boff);
+#pragma unroll
+            for (int k = 0; k < KA * 4; ++k) {
+              const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
               if constexpr (KIND == TcKind::I8)
-                mma_i8_ss(dcol, ad, bd, kIdesc, k > 0 ? 1u : 0u);
+                mma_i8_ss(dcol, ad0 + koff, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
               else
-                mma_f16_ss(dcol, ad, bd, kIdesc, k > 0 ? 1u : 0u);
+                mma_f16_ss(dcol, ad0 + koff, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
             }
             mma_commit(&hdr->tfull[slot]);
-            if (++slot == kSlots) {
-              slot = 0;
-              sphase ^= 1;
-            }
           }
-          mma_commit(&hdr->empty[stage]);
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&hdr->empty[stage]);
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -261,7 +330,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int quad = (int)(warp & 3);
     const int row_local = quad * 32 + (int)lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    uint32_t nslot = 0;  // accumulator slots consumed so far (by both sets), gives slot + phase
+    uint32_t uses = 0;  // slot uses by this set: slot = wset + 2 * (uses & 1), parity = (uses >> 1) & 1
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
       decode_unit(u, p, q, g, b);
@@ -287,13 +356,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int i = 0; i < 2; ++i) {
           const int mb = 2 * i + wset;
           if (mb >= qbv) break;
-          const uint32_t n = nslot + (uint32_t)mb;
-          const uint32_t slot = n % kSlots, sphase = (n / kSlots) & 1u;
+          const uint32_t slot = (uint32_t)wset + 2u * (uses & 1u), sphase = (uses >> 1) & 1u;
+          ++uses;
           mbar_wait(&hdr->tfull[slot], sphase);
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + slot * 128u;
           const int base = t * kTileRows;
-          if (p.debug) {
+          if (p.debug == 1 || p.debug == 2) {
             if (p.debug == 1) {
               uint32_t ra[32], rb[32];
               tmem_ld32(taddr, ra);
@@ -339,7 +408,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             epi_chunk<KIND>(rd, base + 96, vl, p, b, sq[i], m[i], ix[i]);
           }
         }
-        nslot += (uint32_t)qbv;
       }
       const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
 #pragma unroll

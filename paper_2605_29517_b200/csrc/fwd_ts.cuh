@@ -1,0 +1,361 @@
+// Flash-MaxSim dense forward, v3: query resident in TMEM (tcgen05 "TS" MMA), document tiles
+// multicast across a CTA cluster, per-row best-chunk stash for the argmax.
+//
+// Same contract as fwd_tc.cuh (maxsim/forward.py:108-155 _fold_pair; S2 masking, S3 strict-> /
+// lowest index) -- only the data movement differs:
+//   * Q row group (<= 4 blocks x 128 rows) lives in TMEM columns [0, 256): the MMA reads A
+//     from TMEM and only the document tile B from shared memory (half the smem feed of SS);
+//   * accumulators: two 128-column slots in TMEM columns [256, 512), slot = Q block parity;
+//   * a cluster of CL CTAs (one per Q row group) scores the same documents in lockstep; each
+//     CTA TMA-loads 128/CL rows of every 128-token document tile and multicasts them to the
+//     whole cluster, so a document byte leaves L2 once (not once per Q row group);
+//   * argmax: the epilogue keeps only a running max per row plus, for lanes that improve, a
+//     copy of the improving 32-column chunk in shared memory.  The lowest index attaining the
+//     final max is resolved once per (row, document) from that copy -- no per-chunk rescans
+//     across the warp.
+#pragma once
+#include "fwd_tc.cuh"
+
+namespace mxs {
+
+constexpr int kTsAccCol0 = 256;  // accumulator slots start here
+constexpr int kTsSlots = 2;
+
+struct TsSmemHeader {
+  uint64_t full[8];
+  uint64_t empty[8];
+  uint64_t tfull[kTsSlots];
+  uint64_t tempty[kTsSlots];
+  uint64_t qfull;
+  uint64_t qempty;
+  uint32_t tmem_base;
+  uint32_t pad;
+};
+
+__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages) {
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128 + sizeof(TsSmemHeader);
+}
+
+// Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
+// that a warp's predicated stores spread over all banks.
+MXS_DEV void stash_chunk(float* row128, const float (&v)[32], int swz) {
+  float4* dst = reinterpret_cast<float4*>(row128);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dst[i ^ swz] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+MXS_DEV void unstash_chunk(const float* row128, float (&v)[32], int swz) {
+  const float4* src = reinterpret_cast<const float4*>(row128);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 t = src[i ^ swz];
+    v[4 * i] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+  }
+}
+
+template <TcKind KIND>
+MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcParams& p, int b, float sq, float& m,
+                      int& cb, float* stash_row, int swz) {
+  if (base >= vl) return;
+  float v[32];
+  if constexpr (KIND == TcKind::I8) {
+    const float* sd = p.d_scale + (long long)b * p.l_pad + base;
+    const bool full = base + 32 <= p.l_pad;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float sdj = (full || base + j < p.l_pad) ? __ldg(sd + j) : 1.f;
+      v[j] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), sq), sdj);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  }
+  if (base + 32 > vl) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (base + j >= vl) v[j] = -INFINITY;
+  }
+  const float cmax = max32(v);
+  const bool upd = cmax > m;
+  if (__any_sync(0xffffffffu, upd)) {
+    if (upd) {
+      m = cmax;
+      cb = base;
+      stash_chunk(stash_row, v, swz);
+    }
+  }
+}
+
+template <TcKind KIND, int KA, int CL>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fwd_ts_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sD = smem;
+  float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
+  TsSmemHeader* hdr = reinterpret_cast<TsSmemHeader*>(reinterpret_cast<uint8_t*>(sBest) + (size_t)p.qb * 128 * 128);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int crank = (CL > 1) ? (int)cluster_ctarank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+  constexpr int kQCols = KA * 32;  // TMEM columns per Q block (128 B atoms / 4 B per column)
+
+  // unit ranges: with a cluster, units are (q, b) and the Q row group is the CTA rank
+  const long long n_workers = gridDim.x / CL;
+  const long long worker = blockIdx.x / CL;
+  const long long per = p.n_units / n_workers, rem = p.n_units % n_workers;
+  const long long u_begin = worker * per + min(worker, rem);
+  const long long u_end = u_begin + per + (worker < rem ? 1 : 0);
+  const int nmb_total = (p.l_q + kTileRows - 1) / kTileRows;
+  auto decode = [&](long long u, int& q, int& g, int& b) {
+    if (CL > 1) {
+      b = (int)(u % p.n_docs);
+      q = (int)(u / p.n_docs);
+      g = crank;
+    } else {
+      decode_unit(u, p, q, g, b);
+    }
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmD);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&hdr->full[s], 1);
+      mbar_init(&hdr->empty[s], CL);
+    }
+    for (int s = 0; s < kTsSlots; ++s) {
+      mbar_init(&hdr->tfull[s], 1);
+      mbar_init(&hdr->tempty[s], 4);
+    }
+    mbar_init(&hdr->qfull, kEpiWarps);
+    mbar_init(&hdr->qempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&hdr->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  if (CL > 1) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = hdr->tmem_base;
+
+  constexpr uint32_t kIdesc = (KIND == TcKind::I8) ? make_idesc(2, 1, 128, 128)
+                              : (KIND == TcKind::BF16) ? make_idesc(1, 1, 128, 128)
+                                                       : make_idesc(1, 0, 128, 128);
+  constexpr int kElemsPerAtom = (KIND == TcKind::I8) ? 128 : 64;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      constexpr int kRowsPer = kTileRows / CL;
+      for (long long u = u_begin; u < u_end; ++u) {
+        int q, g, b;
+        decode(u, q, g, b);
+        const int vl = doc_valid_len(p, b);
+        const int ntiles = (vl + kTileRows - 1) / kTileRows;
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(&hdr->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
+          const int row0 = b * p.l_pad + t * kTileRows + crank * kRowsPer;
+#pragma unroll
+          for (int a = 0; a < KA; ++a) {
+            uint8_t* dst = sD + (size_t)(stage * KA + a) * kAtomBytes + crank * kRowsPer * 128;
+            if (CL > 1)
+              tma_load_2d_mc(&tmD, &hdr->full[stage], dst, a * kElemsPerAtom, row0, kMask, kEvictFirst);
+            else
+              tma_load_2d(&tmD, &hdr->full[stage], dst, a * kElemsPerAtom, row0, kEvictFirst);
+          }
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (TS)
+    // Accumulator slot = Q block parity, so each epilogue warp set (which owns the blocks of
+    // one parity) consumes every phase of its own slot in order -- a waiter can never be two
+    // phases behind and alias an mbarrier parity.
+    int stage = 0;
+    uint32_t phase = 0, qphase = 0;
+    uint32_t sphase[kTsSlots] = {0u, 0u};
+    long long cur_key = -1;
+    const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
+    for (long long u = u_begin; u < u_end; ++u) {
+      int q, g, b;
+      decode(u, q, g, b);
+      const long long key = (long long)q * p.n_groups + g;
+      if (key != cur_key) {
+        if (cur_key >= 0) {
+          if (elect_one()) mma_commit(&hdr->qempty);
+          __syncwarp();
+        }
+        mbar_wait(&hdr->qfull, qphase);
+        qphase ^= 1;
+        tc_fence_after();
+        cur_key = key;
+      }
+      const int qbv = min(p.qb, nmb_total - g * p.qb);
+      const int vl = doc_valid_len(p, b);
+      const int ntiles = (vl + kTileRows - 1) / kTileRows;
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait(&hdr->full[stage], phase);
+        tc_fence_after();
+        const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
+        for (int mb = 0; mb < qbv; ++mb) {
+          const int slot = mb & 1;
+          mbar_wait(&hdr->tempty[slot], sphase[slot] ^ 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
+            const uint32_t dcol = tmem_base + (uint32_t)(kTsAccCol0 + slot * 128);
+#pragma unroll
+            for (int k = 0; k < KA * 4; ++k) {
+              const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
+              if constexpr (KIND == TcKind::I8)
+                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+              else
+                mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+            }
+            mma_commit(&hdr->tfull[slot]);
+          }
+          __syncwarp();
+          sphase[slot] ^= 1;
+        }
+        if (elect_one()) {
+          if (CL > 1)
+            mma_commit_mc(&hdr->empty[stage], kMask);
+          else
+            mma_commit(&hdr->empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
+    const int wset = ((int)warp - 4) >> 2;
+    const int quad = (int)(warp & 3);
+    const int row_local = quad * 32 + (int)lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const int swz = (int)(lane & 7);
+    const int eb = (KIND == TcKind::I8) ? 1 : 2;
+    const int row_bytes = p.dim * eb;
+    uint32_t sph = 0, qeph = 0;  // this set's slot is `wset`; sph = parity of its next use
+    long long cur_key = -1;
+    for (long long u = u_begin; u < u_end; ++u) {
+      int q, g, b;
+      decode(u, q, g, b);
+      const int qbv = min(p.qb, nmb_total - g * p.qb);
+      const long long key = (long long)q * p.n_groups + g;
+      if (key != cur_key) {
+        if (cur_key >= 0) {
+          mbar_wait(&hdr->qempty, qeph);  // every MMA reading the old Q block has completed
+          qeph ^= 1;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int mb = 2 * i + wset;
+          if (mb >= qbv) break;
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          const uint8_t* src = static_cast<const uint8_t*>(p.q_ptr) + ((long long)q * p.l_q + row) * row_bytes;
+#pragma unroll
+          for (int a = 0; a < KA; ++a) {
+            uint32_t r[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int off = a * 128 + c * 16;
+              uint4 w = make_uint4(0u, 0u, 0u, 0u);
+              if (row < p.l_q && off < row_bytes) w = __ldg(reinterpret_cast<const uint4*>(src + off));
+              r[4 * c] = w.x;
+              r[4 * c + 1] = w.y;
+              r[4 * c + 2] = w.z;
+              r[4 * c + 3] = w.w;
+            }
+            tmem_st32(tmem_base + lane_base + (uint32_t)(mb * kQCols + a * 32), r);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hdr->qfull);
+        cur_key = key;
+      }
+      const int vl = doc_valid_len(p, b);
+      const int ntiles = (vl + kTileRows - 1) / kTileRows;
+      float m[2], sq[2];
+      int cb[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        m[i] = -INFINITY;
+        cb[i] = 0;
+        sq[i] = 1.f;
+        if constexpr (KIND == TcKind::I8) {
+          const int mb = 2 * i + wset;
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          if (mb < qbv && row < p.l_q) sq[i] = __ldg(p.q_scale + (long long)q * p.l_q + row);
+        }
+      }
+      for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int mb = 2 * i + wset;
+          if (mb >= qbv) break;
+          const uint32_t slot = (uint32_t)wset;
+          mbar_wait(&hdr->tfull[slot], sph);
+          sph ^= 1u;
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kTsAccCol0 + slot * 128);
+          uint32_t ra[32], rb[32], rc[32], rd[32];
+          tmem_ld32(taddr, ra);
+          tmem_ld32(taddr + 32, rb);
+          tmem_ld32(taddr + 64, rc);
+          tmem_ld32(taddr + 96, rd);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+          float* stash = sBest + ((size_t)mb * 128 + row_local) * 32;
+          const int base = t * kTileRows;
+          ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          ts_chunk<KIND>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          ts_chunk<KIND>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+        }
+      }
+      const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int mb = 2 * i + wset;
+        if (mb >= qbv) break;
+        const int row = (g * p.qb + mb) * kTileRows + row_local;
+        if (row < p.l_q) {
+          p.rowmax[obase + row] = m[i];
+          if (p.argmax) {
+            float w[32];
+            unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * 32, w, swz);
+            p.argmax[obase + row] = cb[i] + first_argmax32_chain(w, m[i]);
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (CL > 1) cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace mxs
