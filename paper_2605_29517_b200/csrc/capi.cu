@@ -215,7 +215,7 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   if (workers <= 0) return MXS_OK;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(workers * cl));
-  cfg.blockDim = dim3(mxs::kFwdThreads);
+  cfg.blockDim = dim3(mxs::kTsThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

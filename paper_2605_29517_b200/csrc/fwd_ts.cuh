@@ -20,6 +20,8 @@ namespace mxs {
 
 constexpr int kTsAccCol0 = 256;  // accumulator slots start here
 constexpr int kTsSlots = 2;
+constexpr int kTsEpiWarp0 = 2;                               // warps 2..9: epilogue
+constexpr int kTsThreads = 32 * (kTsEpiWarp0 + kEpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM alloc
 
 struct TsSmemHeader {
   uint64_t full[8];
@@ -89,7 +91,7 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
 }
 
 template <TcKind KIND, int KA, int CL>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __launch_bounds__(kTsThreads, 1)
     fwd_ts_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_init(&hdr->qempty, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(&hdr->tmem_base, 512);
+  if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // phases behind and alias an mbarrier parity.
     int stage = 0;
     uint32_t phase = 0, qphase = 0;
-    uint32_t sphase[kTsSlots] = {0u, 0u};
+    uint32_t sbits = 0;  // bit s = parity of slot s's next use
     long long cur_key = -1;
     const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
     for (long long u = u_begin; u < u_end; ++u) {
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
         for (int mb = 0; mb < qbv; ++mb) {
           const int slot = mb & 1;
-          mbar_wait(&hdr->tempty[slot], sphase[slot] ^ 1);
+          mbar_wait(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             mma_commit(&hdr->tfull[slot]);
           }
           __syncwarp();
-          sphase[slot] ^= 1;
+          sbits ^= 1u << slot;
         }
         if (elect_one()) {
           if (CL > 1)
@@ -240,9 +242,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
-    const int wset = ((int)warp - 4) >> 2;
+    // warp w in [2, 10): TMEM lane quadrant w % 4 (hardware rule), set (w - 2) / 4.
+    const int wset = ((int)warp - kTsEpiWarp0) >> 2;
     const int quad = (int)(warp & 3);
     const int row_local = quad * 32 + (int)lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
