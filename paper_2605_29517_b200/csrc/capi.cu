@@ -11,6 +11,7 @@
 #include "fwd_exact.cuh"
 #include "fwd_tc.cuh"
 #include "fwd_ts.cuh"
+#include "varlen_tc.cuh"
 #include "csr.cuh"
 #include "grad.cuh"
 #include "quant.cuh"
@@ -230,6 +231,57 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   return check_launch("fwd_ts_kernel");
 }
 
+template <mxs::TcKind KIND>
+int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens, const int64_t* cu, int64_t n_docs,
+                     int64_t n_tokens, int64_t dim, float* rowmax, int32_t* argmax, cudaStream_t st) {
+  const int eb = (KIND == mxs::TcKind::I8) ? 1 : 2;
+  const long long n_cols = n_q * l_q;
+  if (n_cols > 128 || (dim * eb) % 16 != 0) return MXS_UNSUPPORTED;
+  const int ka = (int)((dim * eb + 127) / 128);
+  if (ka > 4) return MXS_UNSUPPORTED;
+  const int ncp = (int)((n_cols + 15) / 16) * 16;
+  const size_t max_smem = 232448;
+  const size_t fixed = 1024 + sizeof(mxs::VlSmemHeader) + (size_t)ka * ncp * 128;
+  int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
+  if (stages > 8) stages = 8;
+  if (stages < 2) return MXS_UNSUPPORTED;
+  mxs::VarlenParams p = {};
+  p.n_q = (int)n_q;
+  p.l_q = (int)l_q;
+  p.n_cols = (int)n_cols;
+  p.n_cols_pad = ncp;
+  p.n_docs = n_docs;
+  p.n_tokens = n_tokens;
+  p.dim = (int)dim;
+  p.stages = stages;
+  p.cu = (const long long*)cu;
+  p.rowmax = rowmax;
+  p.argmax = argmax;
+  const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tt, tq;
+  int s;
+  if ((s = make_tmap_2d(&tt, tokens, dt, eb, dim, n_tokens)) != MXS_OK) return s;
+  if ((s = make_tmap_2d(&tq, Q, dt, eb, dim, n_cols, ncp)) != MXS_OK) return s;
+  const size_t smem = mxs::varlen_smem_bytes(ka, stages, ncp);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::VarlenParams) = nullptr;
+  switch (ka) {
+    case 1: kern = mxs::varlen_tc_kernel<KIND, 1>; break;
+    case 2: kern = mxs::varlen_tc_kernel<KIND, 2>; break;
+    case 3: kern = mxs::varlen_tc_kernel<KIND, 3>; break;
+    case 4: kern = mxs::varlen_tc_kernel<KIND, 4>; break;
+    default: return MXS_UNSUPPORTED;
+  }
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
+  const int nsm = sm_count();
+  if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
+  const long long grid = n_docs < nsm ? n_docs : nsm;
+  kern<<<(unsigned)grid, mxs::kVlThreads, smem, st>>>(tt, tq, p);
+  return check_launch("varlen_tc_kernel");
+}
+
 bool use_ts_path() {
   const char* impl = getenv("MXS_FWD_IMPL");
   return !(impl && strcmp(impl, "ss") == 0);
@@ -256,6 +308,36 @@ int launch_fwd_exact(const void* Q, int64_t n_q, int64_t l_q, const void* D, int
   mxs::fwd_exact_kernel<T><<<(unsigned)grid, mxs::kExThreads, 0, st>>>(static_cast<const T*>(Q),
                                                                         static_cast<const T*>(D), p);
   return check_launch("fwd_exact_kernel");
+}
+
+
+// Vectorised gather dispatch: rows must be 8-byte aligned (dim * sizeof(T) % 8 == 0) and the
+// dimension must fit NP <= 4 passes of 32 lanes x 8 bytes; otherwise the scalar kernels run.
+template <typename T>
+static bool launch_grad_docs_vec(const T* Q, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  constexpr int V = mxs::Vec8<T>::N;
+  if ((p.dim * (int)sizeof(T)) % 8 != 0) return false;
+  const int np = (p.dim + 32 * V - 1) / (32 * V);
+  switch (np) {
+    case 1: mxs::grad_docs_vec_kernel<T, 1><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    case 2: mxs::grad_docs_vec_kernel<T, 2><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    case 3: mxs::grad_docs_vec_kernel<T, 3><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    case 4: mxs::grad_docs_vec_kernel<T, 4><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    default: return false;
+  }
+}
+template <typename T>
+static bool launch_grad_query_vec(const T* D, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  constexpr int V = mxs::Vec8<T>::N;
+  if ((p.dim * (int)sizeof(T)) % 8 != 0) return false;
+  const int np = (p.dim + 32 * V - 1) / (32 * V);
+  switch (np) {
+    case 1: mxs::grad_query_vec_kernel<T, 1><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    case 2: mxs::grad_query_vec_kernel<T, 2><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    case 3: mxs::grad_query_vec_kernel<T, 3><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    case 4: mxs::grad_query_vec_kernel<T, 4><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    default: return false;
+  }
 }
 
 }  // namespace
@@ -446,13 +528,16 @@ int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
   p.dD = dD;
   cudaStream_t st = (cudaStream_t)stream;
   const long long blocks = (n_dest * 32 + 255) / 256;
-  if (dtype == MXS_F32)
-    mxs::grad_docs_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)Q, p);
-  else if (dtype == MXS_BF16)
-    mxs::grad_docs_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)Q, p);
-  else if (dtype == MXS_F16)
-    mxs::grad_docs_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)Q, p);
-  else
+  if (dtype == MXS_F32) {
+    if (!launch_grad_docs_vec<float>((const float*)Q, p, blocks, st))
+      mxs::grad_docs_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)Q, p);
+  } else if (dtype == MXS_BF16) {
+    if (!launch_grad_docs_vec<__nv_bfloat16>((const __nv_bfloat16*)Q, p, blocks, st))
+      mxs::grad_docs_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)Q, p);
+  } else if (dtype == MXS_F16) {
+    if (!launch_grad_docs_vec<__half>((const __half*)Q, p, blocks, st))
+      mxs::grad_docs_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)Q, p);
+  } else
     return fail(MXS_UNSUPPORTED, "mxs_grad_docs_csr: dtype %d", dtype);
   return check_launch("grad_docs_kernel");
 }
@@ -473,22 +558,63 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
   cudaStream_t st = (cudaStream_t)stream;
   const long long blocks = (n_q * l_q * 32 + 255) / 256;
   if (blocks == 0) return MXS_OK;
-  if (dtype == MXS_F32)
-    mxs::grad_query_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)D, p);
-  else if (dtype == MXS_BF16)
-    mxs::grad_query_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)D, p);
-  else if (dtype == MXS_F16)
-    mxs::grad_query_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)D, p);
-  else
+  if (dtype == MXS_F32) {
+    if (!launch_grad_query_vec<float>((const float*)D, p, blocks, st))
+      mxs::grad_query_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)D, p);
+  } else if (dtype == MXS_BF16) {
+    if (!launch_grad_query_vec<__nv_bfloat16>((const __nv_bfloat16*)D, p, blocks, st))
+      mxs::grad_query_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)D, p);
+  } else if (dtype == MXS_F16) {
+    if (!launch_grad_query_vec<__half>((const __half*)D, p, blocks, st))
+      mxs::grad_query_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)D, p);
+  } else
     return fail(MXS_UNSUPPORTED, "mxs_grad_query: dtype %d", dtype);
   return check_launch("grad_query_kernel");
 }
 
-static const long long kTopkChunk = 8192;
+static const long long kTopkChunk = mxs::kTopkSlice;
+static const size_t kTopkSmem = mxs::kTopkSlice * (sizeof(double) + sizeof(long long));
+
+// Passes until one block remains: each pass keeps k candidates per 8192-element slice.
+static long long topk_ws_elems(long long n, long long k) {
+  long long total = 0;
+  while (n > kTopkChunk) {
+    const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+    n = blocks * k;
+    total += n;
+  }
+  return total;
+}
+
+static int topk_run(const double* s, const long long* ids, long long n, long long k, long long id_offset, double* top_s,
+                    long long* top_id, void* ws, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(mxs::topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkSmem);
+  });
+  double* cs = (double*)ws;
+  const long long cap = topk_ws_elems(n, k);
+  long long* ci = (long long*)(cs + cap);
+  long long used = 0;
+  while (n > kTopkChunk) {
+    const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+    double* os = cs + used;
+    long long* oi = ci + used;
+    mxs::topk_kernel<<<(unsigned)blocks, mxs::kTopkThreads, kTopkSmem, st>>>(s, ids, n, (int)k, kTopkChunk, id_offset, os, oi);
+    int r;
+    if ((r = check_launch("topk_kernel")) != MXS_OK) return r;
+    s = os;
+    ids = oi;
+    id_offset = 0;
+    n = blocks * k;
+    used += n;
+  }
+  mxs::topk_kernel<<<1, mxs::kTopkThreads, kTopkSmem, st>>>(s, ids, n, (int)k, n, id_offset, top_s, top_id);
+  return check_launch("topk_kernel");
+}
 
 size_t mxs_topk_workspace_bytes(int64_t n, int64_t k) {
-  const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
-  return (size_t)(blocks * k) * (sizeof(double) + sizeof(long long));
+  return (size_t)topk_ws_elems(n, k) * (sizeof(double) + sizeof(long long));
 }
 
 int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, double* top_s, int64_t* top_id, void* ws,
@@ -496,23 +622,20 @@ int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, doub
   if (!scores || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk: null pointer");
   if (k > n) return fail(MXS_K_TOO_LARGE, "top-%lld requested from a corpus of %lld documents", (long long)k, (long long)n);
   if (k <= 0) return MXS_OK;
-  if (k > 4096) return fail(MXS_UNSUPPORTED, "mxs_topk: k > 4096");
-  cudaStream_t st = (cudaStream_t)stream;
-  const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
-  if (blocks == 1) {
-    mxs::topk_kernel<<<1, 512, 0, st>>>(scores, nullptr, n, (int)k, n, id_offset, top_s, (long long*)top_id);
-    return check_launch("topk_kernel");
-  }
-  if (!ws || ws_bytes < mxs_topk_workspace_bytes(n, k)) return fail(MXS_INVALID_ARGUMENT, "mxs_topk: workspace too small");
-  double* cs = (double*)ws;
-  long long* ci = (long long*)(cs + blocks * k);
-  mxs::topk_kernel<<<(unsigned)blocks, 512, 0, st>>>(scores, nullptr, n, (int)k, kTopkChunk, id_offset, cs, ci);
-  int s;
-  if ((s = check_launch("topk_kernel")) != MXS_OK) return s;
-  mxs::topk_kernel<<<1, 512, 0, st>>>(cs, ci, blocks * k, (int)k, blocks * k, 0, top_s, (long long*)top_id);
-  return check_launch("topk_kernel");
+  if (k > 2048) return fail(MXS_UNSUPPORTED, "mxs_topk: k > 2048");
+  if (mxs_topk_workspace_bytes(n, k) > 0 && (!ws || ws_bytes < mxs_topk_workspace_bytes(n, k)))
+    return fail(MXS_INVALID_ARGUMENT, "mxs_topk: workspace too small");
+  return topk_run(scores, nullptr, n, k, id_offset, top_s, (long long*)top_id, ws, (cudaStream_t)stream);
 }
 
+int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
+                        void* stream) {
+  if (!scores || !ids || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk_candidates: null pointer");
+  if (k <= 0) return MXS_OK;
+  if (k > 2048) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: k > 2048");
+  if (n > kTopkChunk) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: more than 4096 candidates");
+  return topk_run(scores, (const long long*)ids, n, k, 0, top_s, (long long*)top_id, nullptr, (cudaStream_t)stream);
+}
 
 int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* tokens,
                            const int64_t* cu_seqlens, int64_t n_docs, int64_t n_tokens, int64_t dim, double* scores,
@@ -522,9 +645,14 @@ int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
   if (n_q < 1 || n_docs < 1 || l_q < 1 || dim < 1 || n_tokens < 1)
     return fail(MXS_SHAPE_MISMATCH, "mxs_fused_score_varlen: non-positive shape");
   cudaStream_t st = (cudaStream_t)stream;
-  int s;
-  (void)exact;
+  int s = MXS_UNSUPPORTED;
   const long long* cu = (const long long*)cu_seqlens;
+  if (!exact && dtype == MXS_BF16)
+    s = launch_varlen_tc<mxs::TcKind::BF16>(Q, n_q, l_q, tokens, cu_seqlens, n_docs, n_tokens, dim, rowmax, argmax, st);
+  else if (!exact && dtype == MXS_F16)
+    s = launch_varlen_tc<mxs::TcKind::F16>(Q, n_q, l_q, tokens, cu_seqlens, n_docs, n_tokens, dim, rowmax, argmax, st);
+  if (s == MXS_OK) return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
+  if (s != MXS_UNSUPPORTED) return s;
   if (dtype == MXS_F32)
     s = launch_fwd_exact<float>(Q, n_q, l_q, tokens, n_docs, 0, dim, nullptr, cu, rowmax, argmax, st);
   else if (dtype == MXS_BF16)
@@ -535,17 +663,6 @@ int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     return fail(MXS_UNSUPPORTED, "mxs_fused_score_varlen: dtype %d", dtype);
   if (s != MXS_OK) return s;
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
-}
-
-
-int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
-                        void* stream) {
-  if (!scores || !ids || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk_candidates: null pointer");
-  if (k <= 0) return MXS_OK;
-  if (k > 4096) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: k > 4096");
-  mxs::topk_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(scores, (const long long*)ids, n, (int)k, n, 0, top_s,
-                                                        (long long*)top_id);
-  return check_launch("topk_kernel");
 }
 
 }  // extern "C"

@@ -121,30 +121,52 @@ __global__ void __launch_bounds__(kExThreads) fwd_exact_kernel(const T* __restri
   }
 }
 
-// Per-pair score: strict left-to-right float64 sum of the fp32 row maxima (S4,
-// `maxsim/kernels.py:22-26` seq_sum_f64).  One warp per pair; every lane carries the same
-// running sum so the chain is sequential without divergence.
+// Per-pair score: the strict left-to-right float64 sum of the fp32 row maxima (S4,
+// `maxsim/kernels.py:22-26` seq_sum_f64), computed in parallel when that is provably identical.
+//
+// Every fp32 value is a multiple of its ulp 2^(E-150) (E = biased exponent, 1 for subnormals)
+// and smaller than 2^(E-126).  If Emax - Emin <= 29 - ceil(log2 n), every partial sum of any
+// subset is a multiple of 2^(Emin-150) below 2^(53+Emin-150): exactly representable in f64.
+// Then the sequential sum and any tree sum are both the exact sum -- bit-identical.  Pairs that
+// fail the certificate (maxima spanning > 2^19 in magnitude) take the sequential chain.
+// One warp per pair; lanes stride the row maxima (coalesced).
 __global__ void rowsum_kernel(const float* __restrict__ rowmax, long long n_pairs, int l_q, double* __restrict__ scores) {
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_pairs) return;
   const float* r = rowmax + warp * l_q;
   double s = 0.0;
-  bool first = true;
-  for (int c = 0; c < l_q; c += 32) {
-    const float v = (c + lane < l_q) ? r[c + lane] : 0.f;
-    const int nv = min(32, l_q - c);
-    for (int j = 0; j < nv; ++j) {
-      const double x = (double)__shfl_sync(0xffffffffu, v, j);
-      if (first) {
-        s = x;
-        first = false;
-      } else {
-        s = __dadd_rn(s, x);
-      }
+  int emin = 255, emax = 0;
+  bool finite = true;
+  for (int i = lane; i < l_q; i += 32) {
+    const float v = __ldg(r + i);
+    const uint32_t bits = __float_as_uint(v) & 0x7fffffffu;
+    if (bits >= 0x7f800000u) finite = false;
+    if (bits != 0u) {
+      const int e = max((int)(bits >> 23), 1);
+      emin = min(emin, e);
+      emax = max(emax, e);
     }
+    s += (double)v;
   }
-  if (lane == 0) scores[warp] = s;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  finite = __all_sync(0xffffffffu, finite);
+  const int log2n = 32 - __clz(max(l_q - 1, 1));
+  const bool exact = finite && (emax == 0 || emax - emin <= 29 - log2n);
+  if (exact) {
+    if (lane == 0) scores[warp] = s;
+    return;
+  }
+  if (lane == 0) {  // sequential fallback (rare): the reference order itself
+    double t = (double)r[0];
+    for (int i = 1; i < l_q; ++i) t = __dadd_rn(t, (double)r[i]);
+    scores[warp] = t;
+  }
 }
 
 }  // namespace mxs

@@ -63,12 +63,31 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
   if (base >= vl) return;
   float v[32];
   if constexpr (KIND == TcKind::I8) {
+    // fl(fl(f32(acc) * s_q) * s_d) in the order of maxsim/quant.py:174-176 (S7).
     const float* sd = p.d_scale + (long long)b * p.l_pad + base;
-    const bool full = base + 32 <= p.l_pad;
+    const bool vec = (base + 32 <= p.l_pad) && ((p.l_pad & 3) == 0);
+    float sdv[32];
+    if (vec) {
+      const float4* sd4 = reinterpret_cast<const float4*>(sd);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float sdj = (full || base + j < p.l_pad) ? __ldg(sd + j) : 1.f;
-      v[j] = __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), sq), sdj);
+      for (int c = 0; c < 8; ++c) {
+        const float4 t = __ldg(sd4 + c);
+        sdv[4 * c] = t.x;
+        sdv[4 * c + 1] = t.y;
+        sdv[4 * c + 2] = t.z;
+        sdv[4 * c + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sdv[j] = (base + j < p.l_pad) ? __ldg(sd + j) : 1.f;
+    }
+    // f32(acc): cvt.rn (I2FP); both multiplies as packed FMUL2 pairs (each lane of the pair
+    // rounds exactly like the scalar fl(x * y)).
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      float t0, t1;
+      fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sq, sq);
+      fmul2_rn(v[j], v[j + 1], t0, t1, sdv[j], sdv[j + 1]);
     }
   } else {
 #pragma unroll
@@ -317,21 +336,39 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           sph ^= 1u;
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kTsAccCol0 + slot * 128);
-          uint32_t ra[32], rb[32], rc[32], rd[32];
-          tmem_ld32(taddr, ra);
-          tmem_ld32(taddr + 32, rb);
-          tmem_ld32(taddr + 64, rc);
-          tmem_ld32(taddr + 96, rd);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
           float* stash = sBest + ((size_t)mb * 128 + row_local) * 32;
           const int base = t * kTileRows;
-          ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-          ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-          ts_chunk<KIND>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-          ts_chunk<KIND>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          if constexpr (KIND == TcKind::I8) {
+            // the dequantisation needs extra registers: two chunks in flight at a time
+            uint32_t ra[32], rb[32];
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tmem_ld_wait();
+            ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            tmem_ld32(taddr + 64, ra);
+            tmem_ld32(taddr + 96, rb);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+            ts_chunk<KIND>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          } else {
+            uint32_t ra[32], rb[32], rc[32], rd[32];
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tmem_ld32(taddr + 64, rc);
+            tmem_ld32(taddr + 96, rd);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+            ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+          }
         }
       }
       const long long obase = ((long long)q * p.n_docs + b) * p.l_q;

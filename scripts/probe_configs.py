@@ -1,0 +1,64 @@
+"""Time the non-headline configs: C3 (fwd+bwd), C4 (INT8), C5 (varlen, scaled down), top-K."""
+import ctypes, os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_2605_29517_b200 as mx
+from paper_2605_29517_b200 import _dev, _lib
+from paper_2605_29517_b200.parallel import inbatch_step
+
+def timeit(fn, reps=5, warm=2):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); fn(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2]
+
+g = torch.Generator(device="cuda").manual_seed(0)
+def unit(*shape):
+    x = torch.randn(*shape, device="cuda", generator=g)
+    return (x / x.norm(dim=-1, keepdim=True)).bfloat16()
+
+# C3: in-batch 64 x 64 ColPali shape
+Q = unit(64, 1024, 128); D = unit(64, 1024, 128)
+t_fwd = timeit(lambda: mx.score_dense(Q, D))
+_, am, _ = mx.score_dense(Q, D)
+gq = torch.randn(64, 64, device="cuda", generator=g).float()
+off = torch.arange(64, dtype=torch.int64, device="cuda") * 1024
+lens = torch.full((64,), 1024, dtype=torch.int64, device="cuda")
+from paper_2605_29517_b200.backward import csr_tensors
+from paper_2605_29517_b200.autograd import _grad_docs, _grad_query
+t_csr = timeit(lambda: csr_tensors(am, off, lens, 65536, 1024))
+t_dd = timeit(lambda: _grad_docs(Q, am, gq, off, lens, 65536, 1024, 128))
+t_dq = timeit(lambda: _grad_query(D.reshape(-1, 128), off, am, gq, 128))
+t_step = timeit(lambda: inbatch_step(Q, D, 0))
+print(f"C3 fwd {t_fwd:.3f} ms ({1.0995e12 / t_fwd / 1e9:.0f} TF/s) | csr {t_csr:.3f} | dD {t_dd:.3f} | dQ {t_dq:.3f} | full step {t_step:.3f} ms")
+
+# C4: INT8 10K docs
+nb = 10000
+Qf = unit(1, 1024, 128); Df = torch.empty(nb, 1024, 128, dtype=torch.bfloat16, device="cuda")
+for i in range(0, nb, 1000): Df[i:i + 1000] = unit(1000, 1024, 128)
+t_q = timeit(lambda: mx.quant.quantize_tensor(Df))
+dq, ds = mx.quant.quantize_tensor(Df); qq, qs = mx.quant.quantize_tensor(Qf)
+t_i8 = timeit(lambda: mx.score_int8(qq, qs, dq, ds))
+t_bf = timeit(lambda: mx.score_dense(Qf, Df))
+print(f"C4 int8 {t_i8:.3f} ms ({nb / t_i8 * 1e3 / 1e6:.2f} M docs/s, {2.684e12 / t_i8 / 1e9:.0f} TOP/s) | bf16 {t_bf:.3f} ms | quantize corpus {t_q:.3f} ms")
+del Df, dq
+
+# C5 scaled: varlen 100K docs L in [32, 512], L_q = 32
+rng = np.random.default_rng(0)
+n5 = int(os.environ.get("N5", "100000"))
+lens5 = rng.integers(32, 513, n5)
+cu = torch.from_numpy(np.concatenate([[0], np.cumsum(lens5)])).cuda()
+T = int(cu[-1])
+toks = torch.empty(T, 128, dtype=torch.bfloat16, device="cuda")
+for i in range(0, T, 4_000_000): toks[i:i + 4_000_000] = unit(min(4_000_000, T - i), 128)
+q5 = unit(1, 32, 128)
+t_v = timeit(lambda: mx.score_varlen(q5, toks, cu), reps=3, warm=1)
+byt = T * 256
+print(f"C5 varlen {n5} docs ({T} tokens): {t_v:.3f} ms ({n5 / t_v * 1e3 / 1e6:.2f} M docs/s, {byt / t_v / 1e6:.0f} GB/s)")
+sc, _, _ = mx.score_varlen(q5, toks, cu)
+t_k = timeit(lambda: mx.topk(sc[0], 20))
+print(f"topk 20 of {n5}: {t_k:.3f} ms")

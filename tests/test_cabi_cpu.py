@@ -72,4 +72,5 @@ def test_argument_validation_maps_to_reference_errors(lib):
 
 def test_workspace_sizes(lib):
     assert lib.mxs_csr_workspace_bytes(64, 65536) == 64 * 65536 * 4
-    assert lib.mxs_topk_workspace_bytes(10000, 20) == 2 * 20 * 16
+    assert lib.mxs_topk_workspace_bytes(10000, 20) == 3 * 20 * 16  # 4096-element slices
+    assert lib.mxs_topk_workspace_bytes(4096, 20) == 0

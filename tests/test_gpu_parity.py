@@ -416,3 +416,24 @@ def test_sharded_rerank_merge_equals_global():
     ms, mi = select_candidates(torch.cat(cand_s), torch.cat(cand_i), 20)
     os_, oi = orc.topk(s, 20)
     assert mi.cpu().tolist() == oi.tolist() and ms.cpu().tolist() == os_.tolist()
+
+
+@pytest.mark.parametrize(
+    "n_docs,lo,hi,l_q,n_q",
+    [(300, 32, 512, 32, 1), (1000, 1, 20, 32, 1), (50, 100, 2000, 32, 1), (200, 1, 300, 16, 4), (100, 5, 200, 128, 1),
+     (7, 1, 3, 32, 1)],
+)
+def test_varlen_tensor_core_vs_exact_and_oracle(n_docs, lo, hi, l_q, n_q):
+    """K5 (tcgen05 varlen): documents start/end anywhere in a 128-token tile, 1-token docs, docs
+    spanning many tiles, multi-query column blocks; vs the exact kernel and the oracle."""
+    rng = np.random.default_rng(n_docs + l_q)
+    lens = rng.integers(lo, hi + 1, n_docs)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    toks = cuda(np.concatenate(orc.make_corpus(n_docs, lens, 128, seed=int(rng.integers(1 << 30)))), torch.bfloat16)
+    Q = cuda(orc.make_queries(n_q, l_q, 128, seed=int(rng.integers(1 << 30))), torch.bfloat16)
+    s_tc, a_tc, _ = mx.score_varlen(Q, toks, cuda(cu))
+    s_ex, a_ex, _ = mx.score_varlen(Q, toks, cuda(cu), exact=True)
+    ref_s, ref_a = orc.fused_score_varlen(Q.float().cpu().numpy(), toks.float().cpu().numpy(), cu)
+    assert np.array_equal(s_ex.cpu().numpy(), ref_s) and np.array_equal(a_ex.cpu().numpy(), ref_a)
+    assert rel_err(s_tc.cpu().numpy(), ref_s) < REL
+    assert (a_tc.cpu().numpy() == ref_a).mean() > 0.998
