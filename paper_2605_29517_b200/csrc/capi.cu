@@ -170,8 +170,8 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   const int qb = std::min(qb_max, nmb);
   const int n_groups = (nmb + qb - 1) / qb;
   const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
-  const size_t max_smem = 232448;
-  const size_t fixed = 1024 + sizeof(mxs::TsSmemHeader) + (size_t)qb * 128 * 128;
+  const size_t max_smem = 232448 - sizeof(mxs::TsSmemHeader);  // static header comes out of the same 227 KB
+  const size_t fixed = 1024 + (size_t)qb * 128 * 128;
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
@@ -192,6 +192,10 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   p.rowmax = rowmax;
   p.argmax = argmax;
   p.q_ptr = Q;
+  {
+    const char* dbg = getenv("MXS_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
   CUtensorMap td;
   const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -240,8 +244,8 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
   const int ka = (int)((dim * eb + 127) / 128);
   if (ka > 4) return MXS_UNSUPPORTED;
   const int ncp = (int)((n_cols + 15) / 16) * 16;
-  const size_t max_smem = 232448;
-  const size_t fixed = 1024 + sizeof(mxs::VlSmemHeader) + (size_t)ka * ncp * 128;
+  const size_t max_smem = 232448 - sizeof(mxs::VlSmemHeader);
+  const size_t fixed = 1024 + (size_t)ka * ncp * 128 + sizeof(mxs::VlScratch);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;

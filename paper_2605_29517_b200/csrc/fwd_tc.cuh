@@ -55,8 +55,9 @@ struct FwdSmemHeader {
   uint32_t pad;
 };
 
+// dynamic shared memory (the header is static shared memory)
 __host__ __device__ inline size_t fwd_tc_smem_bytes(int ka, int qb, int stages) {
-  return 1024 /*align slack*/ + (size_t)(qb + stages) * ka * kAtomBytes + sizeof(FwdSmemHeader);
+  return 1024 /*align slack*/ + (size_t)(qb + stages) * ka * kAtomBytes;
 }
 
 MXS_DEV void decode_unit(long long u, const FwdTcParams& p, int& q, int& g, int& b) {
@@ -182,10 +183,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD,
                   const FwdTcParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space,
+  // so accesses compile to LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sD = smem + (size_t)p.qb * KA * kAtomBytes;
-  FwdSmemHeader* hdr = reinterpret_cast<FwdSmemHeader*>(sD + (size_t)p.stages * KA * kAtomBytes);
+  __shared__ FwdSmemHeader tc_hdr;
+  FwdSmemHeader* hdr = &tc_hdr;
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();

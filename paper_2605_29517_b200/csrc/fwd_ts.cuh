@@ -34,8 +34,9 @@ struct TsSmemHeader {
   uint32_t pad;
 };
 
+// dynamic shared memory (the header is static shared memory)
 __host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128 + sizeof(TsSmemHeader);
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128;
 }
 
 // Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
@@ -113,10 +114,13 @@ template <TcKind KIND, int KA, int CL>
 __global__ void __launch_bounds__(kTsThreads, 1)
     fwd_ts_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space,
+  // so accesses compile to LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sD = smem;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
-  TsSmemHeader* hdr = reinterpret_cast<TsSmemHeader*>(reinterpret_cast<uint8_t*>(sBest) + (size_t)p.qb * 128 * 128);
+  __shared__ TsSmemHeader ts_hdr;  // static shared: keeps barrier / bookkeeping accesses on LDS/STS
+  TsSmemHeader* hdr = &ts_hdr;
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
@@ -338,7 +342,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kTsAccCol0 + slot * 128);
           float* stash = sBest + ((size_t)mb * 128 + row_local) * 32;
           const int base = t * kTileRows;
-          if constexpr (KIND == TcKind::I8) {
+          if (p.debug == 2) {  // profiling knob: drain the slot without folding
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+          } else if constexpr (KIND == TcKind::I8) {
             // the dequantisation needs extra registers: two chunks in flight at a time
             uint32_t ra[32], rb[32];
             tmem_ld32(taddr, ra);

@@ -29,9 +29,10 @@ struct VarlenParams {
   int32_t* argmax;      // [n_q, n_docs, l_q] or nullptr
 };
 
-constexpr int kVlEpiWarps = 4;
-constexpr int kVlThreads = 32 * (2 + kVlEpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM alloc, 2..5 epilogue
-constexpr int kVlTilePad = 33;                        // floats per token row of the transpose tile
+constexpr int kVlSets = 2;                            // epilogue warp sets, alternate tiles
+constexpr int kVlEpiWarps = 4 * kVlSets;
+constexpr int kVlThreads = 32 * (2 + kVlEpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM alloc, 2..9 epilogue
+constexpr int kVlTilePad = 36;                        // floats per token row (16-B rows, conflict-free STS.128)
 
 struct VlSmemHeader {
   uint64_t full[8];
@@ -39,22 +40,42 @@ struct VlSmemHeader {
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t qfull;
+  uint64_t carry_ready;  // phase t completes when the ordered merge of tile t is done
   uint32_t tmem_base;
   int32_t doc_begin, doc_end;
   int32_t pad;
   long long tok_begin, tok_end;
-  float tile[128 * kVlTilePad];     // transposed similarities of one 32-column chunk
-  int32_t tok_doc[128];             // document of each token in the tile
-  float hm[4][32];                  // per quarter / column: head piece (max, arg, doc)
-  long long ha[4][32];
-  int32_t hd[4][32];
-  float tm[4][32];                  // tail piece
-  long long ta[4][32];
-  int32_t td[4][32];
 };
 
+// Epilogue scratch in dynamic shared memory, one per warp set (set s owns tiles t = s mod 2).
+constexpr int kVlCuCache = 1280;  // cached cu_seqlens window (documents)
+struct VlPieces {
+  float hm[4][32];
+  float tm[4][32];
+  int32_t hd[4][32];
+  int32_t td[4][32];
+  long long ha[4][32];
+  long long ta[4][32];
+};
+struct VlSetScratch {
+  float tile[128 * kVlTilePad];   // transposed similarities of one 32-column chunk
+  int32_t tok_doc[128];           // document of every token of the tile
+  VlPieces pieces[4];             // per column chunk
+  long long cu_cache[kVlCuCache]; // cu[c0 + j]
+};
+struct VlCarry {                   // ordered-merge state handed from set to set
+  float m[4][32];
+  long long a[4][32];
+  long long d[4][32];
+};
+struct VlScratch {
+  VlSetScratch set[kVlSets];
+  VlCarry carry;
+};
+
+// dynamic shared memory (the small header is static shared memory)
 __host__ __device__ inline size_t varlen_smem_bytes(int ka, int stages, int n_cols_pad) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)ka * n_cols_pad * 128 + sizeof(VlSmemHeader);
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)ka * n_cols_pad * 128 + sizeof(VlScratch);
 }
 
 // first document d in [lo, hi) with cu[d + 1] > tok (i.e. the document containing token tok)
@@ -69,12 +90,13 @@ MXS_DEV long long doc_of_token(const long long* cu, long long lo, long long hi, 
   return lo;
 }
 
-MXS_DEV void vl_emit(const VarlenParams& p, int col, long long doc, float m, long long arg_tok) {
+// arg is already document-local
+MXS_DEV void vl_emit(const VarlenParams& p, int col, long long doc, float m, long long arg) {
   if (doc < 0 || col >= p.n_cols) return;
   const int q = col / p.l_q, i = col % p.l_q;
   const long long o = ((long long)q * p.n_docs + doc) * p.l_q + i;
   p.rowmax[o] = m;
-  if (p.argmax) p.argmax[o] = (int32_t)(arg_tok - __ldg(p.cu + doc));
+  if (p.argmax) p.argmax[o] = (int32_t)arg;
 }
 
 template <TcKind KIND, int KA>
@@ -82,10 +104,14 @@ __global__ void __launch_bounds__(kVlThreads, 1)
     varlen_tc_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmQ,
                      const VarlenParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space,
+  // so accesses compile to LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sT = smem;                                           // token tiles
   uint8_t* sQ = sT + (size_t)p.stages * KA * kAtomBytes;        // all query rows (B operand)
-  VlSmemHeader* hdr = reinterpret_cast<VlSmemHeader*>(sQ + (size_t)KA * p.n_cols_pad * 128);
+  __shared__ VlSmemHeader vl_hdr;  // static shared: keeps every access on the LDS/STS path
+  VlSmemHeader* hdr = &vl_hdr;
+  VlScratch* scr = reinterpret_cast<VlScratch*>(sQ + (size_t)KA * p.n_cols_pad * 128);
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
 
@@ -106,9 +132,10 @@ __global__ void __launch_bounds__(kVlThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&hdr->tfull[s], 1);
-      mbar_init(&hdr->tempty[s], kVlEpiWarps);
+      mbar_init(&hdr->tempty[s], 4);  // the four warps of the set owning the slot
     }
     mbar_init(&hdr->qfull, 1);
+    mbar_init(&hdr->carry_ready, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
@@ -182,50 +209,57 @@ __global__ void __launch_bounds__(kVlThreads, 1)
     }
   } else {
     // ------------------------------------------------------------------ epilogue: segmented max
-    const int ew = (int)warp - 2;                // 0..3 == token quarter
+    const int set = ((int)warp - 2) >> 2;        // warp set: tiles t with t % 2 == set, TMEM slot set
+    const int ew = ((int)warp - 2) & 3;          // token quarter of the scan
     const int quad = (int)(warp & 3);            // TMEM lane quadrant of this warp
-    const int tid = ew * 32 + (int)lane;          // 0..127
+    const int tid = ew * 32 + (int)lane;          // 0..127 within the set
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const int my_tok = quad * 32 + (int)lane;    // token (TMEM lane) this thread loads
-    // carry (merge threads: ew == 0, one column per lane per chunk)
-    float cm[4];
-    long long ca[4];
-    long long cd[4];
+    const long long doc_end = hdr->doc_end;
+    const uint32_t bar_id = 1u + (uint32_t)set;  // named barrier of this set (128 threads)
+    VlSetScratch& S = scr->set[set];
+    VlCarry& C = scr->carry;
+    if (set == 0 && ew == 0) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      cm[c] = -INFINITY;
-      ca[c] = 0;
-      cd[c] = -1;
-    }
-    long long d_lo = hdr->doc_begin;  // first document that can own tokens of the current tile
-    for (int t = 0; t < n_tiles; ++t) {
-      const long long p0 = tok_begin + (long long)t * 128;
-      // ---- document of every token of the tile (start marks + inclusive max scan)
-      {
-        // token 0 belongs to d_lo unless a later document starts exactly at p0 (written after
-        // the barrier, so the two writes never race)
-        const long long d = d_lo + tid;
-        hdr->tok_doc[tid] = (tid == 0) ? (int32_t)d_lo : -1;
-        named_bar_sync(1, 128);
-        if (d < hdr->doc_end) {
-          const long long s = __ldg(p.cu + d) - p0;
-          if (s >= 0 && s < 128) hdr->tok_doc[s] = (int32_t)d;
-        }
-        named_bar_sync(1, 128);
-        int v = hdr->tok_doc[tid];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, v, o);
-          if ((int)lane >= o) v = max(v, y);
-        }
-        if (lane == 31) hdr->td[0][ew] = v;  // scratch for the cross-warp carry
-        named_bar_sync(1, 128);
-        for (int w = 0; w < ew; ++w) v = max(v, hdr->td[0][w]);
-        if (p0 + tid >= tok_end) v = -1;  // tokens past this CTA's range belong to nobody here
-        named_bar_sync(1, 128);
-        hdr->tok_doc[tid] = v;
+      for (int cc = 0; cc < 4; ++cc) {
+        C.m[cc][lane] = -INFINITY;
+        C.a[cc][lane] = 0;
+        C.d[cc][lane] = -1;
       }
-      const int slot = t & 1;
+    }
+    long long lb = hdr->doc_begin;  // lower bound: document of a token at or before this tile
+    long long c0 = -(1LL << 40);    // first document held by this set's cu cache
+    for (int t = set; t < n_tiles; t += kVlSets) {
+      const long long p0 = tok_begin + (long long)t * 128;
+      // ---- cu cache refill (uniform within the set; one global round trip per ~1000 docs)
+      if (lb + 260 > c0 + kVlCuCache) {
+        c0 = lb;
+        for (int j = tid; j < kVlCuCache; j += 128) {
+          const long long d = c0 + j;
+          S.cu_cache[j] = (d <= p.n_docs) ? __ldg(p.cu + d) : LLONG_MAX;
+        }
+        named_bar_sync(bar_id, 128);
+      }
+      // ---- document of this thread's token: binary search of the cached window (no barrier).
+      // At most 257 documents start between the last token of tile t-2 and the end of tile t.
+      {
+        const long long tok = p0 + tid;
+        int dsel = -1;
+        if (tok < tok_end) {
+          long long lo = lb, hi = min(lb + 258, doc_end);  // answer in [lo, hi)
+          while (hi - lo > 1) {
+            const long long mid = (lo + hi) >> 1;
+            if (S.cu_cache[mid - c0] <= tok)
+              lo = mid;
+            else
+              hi = mid;
+          }
+          dsel = (int)lo;
+        }
+        S.tok_doc[tid] = dsel;
+      }
+      int last_doc = -1;
+      const int slot = set;
       mbar_wait(&hdr->tfull[slot], (uint32_t)(t >> 1) & 1u);
       tc_fence_after();
       for (int cc = 0; cc < ncc; ++cc) {
@@ -237,94 +271,117 @@ __global__ void __launch_bounds__(kVlThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
         }
-        float* trow = hdr->tile + my_tok * kVlTilePad;
+        float4* trow = reinterpret_cast<float4*>(S.tile + my_tok * kVlTilePad);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) trow[j] = __uint_as_float(r[j]);
-        named_bar_sync(1, 128);
-        // ---- scan: column c = lane, tokens of quarter ew
+        for (int j = 0; j < 8; ++j)
+          trow[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        named_bar_sync(bar_id, 128);  // (A) transpose tile + token documents visible
+        // read now: after the last barrier of this tile a fast warp may already be rewriting
+        // tok_doc for this set's next tile
+        if (cc == 0) last_doc = S.tok_doc[127];
+        // ---- scan: column c = lane over the 32 tokens of quarter ew, in order
         const int c = (int)lane;
-        float m = -INFINITY;
-        long long a = 0;
-        int cur = -2;
-        int first_doc = -2;
-        bool head_done = false;
-        for (int k = 0; k < 32; ++k) {
-          const int tau = ew * 32 + k;
-          const int d = hdr->tok_doc[tau];
-          if (d != cur) {
-            if (cur != -2) {
-              if (!head_done) {
-                hdr->hm[ew][c] = m;
-                hdr->ha[ew][c] = a;
-                hdr->hd[ew][c] = cur;
-                head_done = true;
-              } else if (cur >= 0) {
-                vl_emit(p, cc * 32 + c, cur, m, a);  // complete inside this quarter
-              }
-            } else {
-              first_doc = d;
-            }
-            cur = d;
-            m = -INFINITY;
-            a = 0;
+        VlPieces& pc = S.pieces[cc];
+        const float* tile = S.tile;
+        const int d_first = S.tok_doc[ew * 32], d_last = S.tok_doc[ew * 32 + 31];
+        if (d_first == d_last) {
+          // fast path (same for all lanes): the quarter lies inside one document -> one piece,
+          // branch-free strict-> fold in token order
+          float m = -INFINITY;
+          int kbest = 0;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float v = tile[(ew * 32 + k) * kVlTilePad + c];
+            const bool up = v > m;
+            m = up ? v : m;
+            kbest = up ? k : kbest;
           }
-          const float v = hdr->tile[tau * kVlTilePad + c];
-          if (v > m) {
-            m = v;
-            a = p0 + tau;
-          }
-        }
-        if (!head_done) {  // the whole quarter is one piece: head == tail
-          hdr->hm[ew][c] = m;
-          hdr->ha[ew][c] = a;
-          hdr->hd[ew][c] = cur;
-          hdr->td[ew][c] = -3;  // marker: no separate tail
+          pc.hm[ew][c] = m;
+          pc.ha[ew][c] = (d_first >= 0) ? p0 + ew * 32 + kbest - S.cu_cache[d_first - c0] : 0;
+          pc.hd[ew][c] = d_first;
+          pc.td[ew][c] = -3;  // marker: no separate tail
         } else {
-          hdr->tm[ew][c] = m;
-          hdr->ta[ew][c] = a;
-          hdr->td[ew][c] = cur;
+          float m = -INFINITY;
+          long long a = 0;
+          int cur = -2;
+          bool head_done = false;
+          for (int k = 0; k < 32; ++k) {
+            const int tau = ew * 32 + k;
+            const int d = S.tok_doc[tau];
+            const float v = tile[tau * kVlTilePad + c];
+            if (d != cur) {
+              if (cur != -2) {
+                const long long al = (cur >= 0) ? a - S.cu_cache[cur - c0] : 0;
+                if (!head_done) {
+                  pc.hm[ew][c] = m;
+                  pc.ha[ew][c] = al;
+                  pc.hd[ew][c] = cur;
+                  head_done = true;
+                } else if (cur >= 0) {
+                  vl_emit(p, cc * 32 + c, cur, m, al);  // document complete inside this quarter
+                }
+              }
+              cur = d;
+              m = -INFINITY;
+              a = 0;
+            }
+            if (v > m) {  // strict: the earliest token wins ties
+              m = v;
+              a = p0 + tau;
+            }
+          }
+          const long long al_last = (cur >= 0) ? a - S.cu_cache[cur - c0] : 0;
+          pc.tm[ew][c] = m;  // head_done is always true here (the document changed)
+          pc.ta[ew][c] = al_last;
+          pc.td[ew][c] = cur;
         }
-        (void)first_doc;
-        named_bar_sync(1, 128);
-        // ---- ordered merge of the quarter pieces with the carry (warp ew == 0)
+        named_bar_sync(bar_id, 128);  // (B) pieces of every quarter visible; tile buffer free
+        // ---- ordered merge (first warp of the set), after the merge of tile t - 1
         if (ew == 0) {
+          if (t > 0) mbar_wait(&hdr->carry_ready, (uint32_t)(t - 1) & 1u);
+          float cm = C.m[cc][c];
+          long long ca = C.a[cc][c], cd = C.d[cc][c];
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const int hd = hdr->hd[h][c];
-            const float hmv = hdr->hm[h][c];
-            const long long hav = hdr->ha[h][c];
-            if (hd == cd[cc]) {
-              if (hmv > cm[cc]) {  // the carry holds earlier tokens: strict > keeps it on ties
-                cm[cc] = hmv;
-                ca[cc] = hav;
+            const int hd = pc.hd[h][c];
+            const float hmv = pc.hm[h][c];
+            const long long hav = pc.ha[h][c];
+            if (hd == cd) {
+              if (hmv > cm) {  // the carry holds earlier tokens: strict > keeps it on ties
+                cm = hmv;
+                ca = hav;
               }
             } else {
-              if (cd[cc] >= 0) vl_emit(p, cc * 32 + c, cd[cc], cm[cc], ca[cc]);
-              cd[cc] = hd;
-              cm[cc] = hmv;
-              ca[cc] = hav;
+              if (cd >= 0) vl_emit(p, cc * 32 + c, cd, cm, ca);
+              cd = hd;
+              cm = hmv;
+              ca = hav;
             }
-            const int tdv = hdr->td[h][c];
-            if (tdv != -3) {  // a document ended inside quarter h; the tail starts a new carry
-              if (cd[cc] >= 0) vl_emit(p, cc * 32 + c, cd[cc], cm[cc], ca[cc]);
-              cd[cc] = tdv;
-              cm[cc] = hdr->tm[h][c];
-              ca[cc] = hdr->ta[h][c];
+            const int tdv = pc.td[h][c];
+            if (tdv != -3) {  // a document ended inside quarter h; its tail starts the new carry
+              if (cd >= 0) vl_emit(p, cc * 32 + c, cd, cm, ca);
+              cd = tdv;
+              cm = pc.tm[h][c];
+              ca = pc.ta[h][c];
             }
           }
+          C.m[cc][c] = cm;
+          C.a[cc][c] = ca;
+          C.d[cc][c] = cd;
+          if (cc == ncc - 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->carry_ready);  // phase t: merge of tile t done
+          }
         }
-        named_bar_sync(1, 128);
       }
-      // next tile starts inside the document of this tile's last token (or the next one)
-      {
-        const int last = hdr->tok_doc[127];
-        if (last >= 0) d_lo = last;
-      }
-      named_bar_sync(1, 128);
+      // this set's next tile starts at or after the document of this tile's last token
+      if (last_doc >= 0) lb = last_doc;
     }
-    if (ew == 0) {
+    // the merge of the last tile flushes the carry
+    if (ew == 0 && n_tiles > 0 && set == ((n_tiles - 1) & 1)) {
       for (int cc = 0; cc < ncc; ++cc)
-        if (cd[cc] >= 0) vl_emit(p, cc * 32 + (int)lane, cd[cc], cm[cc], ca[cc]);
+        if (C.d[cc][lane] >= 0) vl_emit(p, cc * 32 + (int)lane, C.d[cc][lane], C.m[cc][lane], C.a[cc][lane]);
     }
   }
   tc_fence_before();
