@@ -35,8 +35,8 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--docs", type=int, default=10000)
     ap.add_argument("--lq", type=int, default=1024)
@@ -299,7 +299,7 @@ def run_ours(a, rank, world, local_rank):
     sh = _dev.stream_handle(stream)
     doc_offset = rank * nb
     P = _dev.ptr
-    launches_per_step = 1 + 1 + (2 if nb > 8192 else 1) + (1 if world > 1 else 0)
+    launches_per_step = 1 + 1 + (1 if ws_bytes == 0 else 2) + (1 if world > 1 else 0)
 
     def step(Qb, Db, ev=None):
         if ev is not None:
@@ -379,7 +379,7 @@ def run_ours(a, rank, world, local_rank):
         "pct_of_tensor_peak": 100.0 * achieved / peak,
         "roofline": {
             "bound": "tensor",
-            "kernel": "fwd_tc_kernel<BF16> (mxs_fused_rowmax_batch)",
+            "kernel": "fwd_ts_kernel<BF16,KA=2,CL=2> (mxs_fused_rowmax_batch)",
             "achieved": achieved,
             "peak": peak,
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_src})",

@@ -138,7 +138,8 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
  * Top-K selection with the reference ranking: score descending, document id ascending.
  * Replaces maxsim/streamio.py:230 TopKHeap (offer/ranked) and maxsim/cli.py:88 _ranked.
  *   scores [n] f64 -> top_s [k] f64, top_id [k] int64 (= position + id_offset).
- *   ws >= mxs_topk_workspace_bytes(n, k) bytes (may be NULL when n <= 4096); k <= 2048.
+ *   ws >= mxs_topk_workspace_bytes(n, k) bytes (may be NULL when that is 0: n <= 16384 for
+ *   k <= 128, n <= 4096 above); k <= 2048.
  */
 size_t mxs_topk_workspace_bytes(int64_t n, int64_t k);
 int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, double* top_s, int64_t* top_id, void* ws,
@@ -147,6 +148,7 @@ int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, doub
  * Top-K over explicit (score, id) candidates, e.g. the all-gathered per-rank top-K lists of a
  * sharded corpus; entries with id < 0 are empty slots.  Same ordering as mxs_topk
  * (maxsim/streamio.py:255-262 TopKHeap.merge).  Slots beyond the valid candidates get id -1.
+ * n <= 8192 for k <= 128 (n <= 4096 above).
  */
 int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
                         void* stream);

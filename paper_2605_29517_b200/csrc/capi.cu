@@ -171,7 +171,8 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   const int n_groups = (nmb + qb - 1) / qb;
   const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
   const size_t max_smem = 232448 - sizeof(mxs::TsSmemHeader);  // static header comes out of the same 227 KB
-  const size_t fixed = 1024 + (size_t)qb * 128 * 128;
+  const bool scale_ring = (KIND == mxs::TcKind::I8) && (l_pad % 4 == 0);
+  const size_t fixed = mxs::fwd_ts_smem_bytes(0, qb, 0, scale_ring);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
@@ -202,7 +203,7 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
                                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   int s;
   if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
-  const size_t smem = mxs::fwd_ts_smem_bytes(ka, qb, stages);
+  const size_t smem = mxs::fwd_ts_smem_bytes(ka, qb, stages, scale_ring);
   using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
   KernT kern = nullptr;
 #define MXS_TS_CASE(KA_, CL_) \
@@ -579,15 +580,40 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
 static const long long kTopkChunk = mxs::kTopkSlice;
 static const size_t kTopkSmem = mxs::kTopkSlice * (sizeof(double) + sizeof(long long));
 
-// Passes until one block remains: each pass keeps k candidates per 8192-element slice.
-static long long topk_ws_elems(long long n, long long k) {
+static bool use_select(long long k) { return k <= mxs::kSelMaxK; }
+// elements per CTA slice; ids are implicit (positions) only for the first pass of mxs_topk
+static long long topk_slice(long long k, bool explicit_ids) {
+  if (!use_select(k)) return kTopkChunk;
+  return explicit_ids ? mxs::kSelChunkExplicit : mxs::kSelChunkImplicit;
+}
+static size_t select_smem(long long chunk, long long k, bool explicit_ids) {
+  (void)k;
+  return (size_t)chunk * (explicit_ids ? 16 : 8) + (size_t)(mxs::kSelThreads / 32) * mxs::kSelMaxK * 16 +
+         (size_t)mxs::kSelSurvivors * 16;
+}
+
+// Passes until one CTA remains: each pass keeps k candidates per slice.
+static long long topk_ws_elems(long long n, long long k, bool explicit_ids = false) {
   long long total = 0;
-  while (n > kTopkChunk) {
-    const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+  long long slice = topk_slice(k, explicit_ids);
+  while (n > slice) {
+    const long long blocks = (n + slice - 1) / slice;
     n = blocks * k;
     total += n;
+    slice = topk_slice(k, true);
   }
   return total;
+}
+
+static int topk_launch(const double* s, const long long* ids, long long n, long long k, long long blocks,
+                       long long chunk, long long id_offset, double* os, long long* oi, cudaStream_t st) {
+  if (use_select(k)) {
+    mxs::topk_select_kernel<<<(unsigned)blocks, mxs::kSelThreads, select_smem(chunk, k, ids != nullptr), st>>>(
+        s, ids, n, (int)k, chunk, id_offset, os, oi);
+    return check_launch("topk_select_kernel");
+  }
+  mxs::topk_kernel<<<(unsigned)blocks, mxs::kTopkThreads, kTopkSmem, st>>>(s, ids, n, (int)k, chunk, id_offset, os, oi);
+  return check_launch("topk_kernel");
 }
 
 static int topk_run(const double* s, const long long* ids, long long n, long long k, long long id_offset, double* top_s,
@@ -595,26 +621,30 @@ static int topk_run(const double* s, const long long* ids, long long n, long lon
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(mxs::topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkSmem);
+    cudaFuncSetAttribute(mxs::topk_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(select_smem(mxs::kSelChunkImplicit, mxs::kSelMaxK, false),
+                                       select_smem(mxs::kSelChunkExplicit, mxs::kSelMaxK, true)));
   });
   double* cs = (double*)ws;
-  const long long cap = topk_ws_elems(n, k);
+  const long long cap = topk_ws_elems(n, k, ids != nullptr);
   long long* ci = (long long*)(cs + cap);
   long long used = 0;
-  while (n > kTopkChunk) {
-    const long long blocks = (n + kTopkChunk - 1) / kTopkChunk;
+  long long slice = topk_slice(k, ids != nullptr);
+  while (n > slice) {
+    const long long blocks = (n + slice - 1) / slice;
+    const long long chunk = use_select(k) ? (n + blocks - 1) / blocks : slice;  // balanced slices
     double* os = cs + used;
     long long* oi = ci + used;
-    mxs::topk_kernel<<<(unsigned)blocks, mxs::kTopkThreads, kTopkSmem, st>>>(s, ids, n, (int)k, kTopkChunk, id_offset, os, oi);
     int r;
-    if ((r = check_launch("topk_kernel")) != MXS_OK) return r;
+    if ((r = topk_launch(s, ids, n, k, blocks, chunk, id_offset, os, oi, st)) != MXS_OK) return r;
     s = os;
     ids = oi;
     id_offset = 0;
     n = blocks * k;
     used += n;
+    slice = topk_slice(k, true);
   }
-  mxs::topk_kernel<<<1, mxs::kTopkThreads, kTopkSmem, st>>>(s, ids, n, (int)k, n, id_offset, top_s, top_id);
-  return check_launch("topk_kernel");
+  return topk_launch(s, ids, n, k, 1, n, id_offset, top_s, top_id, st);
 }
 
 size_t mxs_topk_workspace_bytes(int64_t n, int64_t k) {
@@ -637,7 +667,8 @@ int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int
   if (!scores || !ids || !top_s || !top_id) return fail(MXS_INVALID_ARGUMENT, "mxs_topk_candidates: null pointer");
   if (k <= 0) return MXS_OK;
   if (k > 2048) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: k > 2048");
-  if (n > kTopkChunk) return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: more than 4096 candidates");
+  if (n > topk_slice(k, true))
+    return fail(MXS_UNSUPPORTED, "mxs_topk_candidates: more than %lld candidates", topk_slice(k, true));
   return topk_run(scores, (const long long*)ids, n, k, 0, top_s, (long long*)top_id, nullptr, (cudaStream_t)stream);
 }
 

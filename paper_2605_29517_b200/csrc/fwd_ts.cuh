@@ -22,6 +22,7 @@ constexpr int kTsAccCol0 = 256;  // accumulator slots start here
 constexpr int kTsSlots = 2;
 constexpr int kTsEpiWarp0 = 2;                               // warps 2..9: epilogue
 constexpr int kTsThreads = 32 * (kTsEpiWarp0 + kEpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM alloc
+constexpr int kScaleSlots = 8;  // INT8: ring of per-tile document scales (128 f32 each) in smem
 
 struct TsSmemHeader {
   uint64_t full[8];
@@ -30,13 +31,16 @@ struct TsSmemHeader {
   uint64_t tempty[kTsSlots];
   uint64_t qfull;
   uint64_t qempty;
+  uint64_t sfull[kScaleSlots];   // INT8 scale ring: TMA bulk copy landed
+  uint64_t sempty[kScaleSlots];  // INT8 scale ring: all 8 epilogue warps done with the tile
   uint32_t tmem_base;
   uint32_t pad;
 };
 
-// dynamic shared memory (the header is static shared memory)
-__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128;
+// dynamic shared memory (the header is static shared memory); `scales` adds the INT8 scale ring
+__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales = false) {
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128 +
+         (scales ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0);
 }
 
 // Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
@@ -58,9 +62,9 @@ MXS_DEV void unstash_chunk(const float* row128, float (&v)[32], int swz) {
   }
 }
 
-template <TcKind KIND>
+template <TcKind KIND, bool kMagic = false>
 MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcParams& p, int b, float sq, float& m,
-                      int& cb, float* stash_row, int swz) {
+                      int& cb, float* stash_row, int swz, const float* sd_smem = nullptr) {
   if (base >= vl) return;
   float v[32];
   if constexpr (KIND == TcKind::I8) {
@@ -68,7 +72,17 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
     const float* sd = p.d_scale + (long long)b * p.l_pad + base;
     const bool vec = (base + 32 <= p.l_pad) && ((p.l_pad & 3) == 0);
     float sdv[32];
-    if (vec) {
+    if (sd_smem) {  // this chunk's 32 scales, staged by the TMA warp (broadcast LDS.128)
+      const float4* s4 = reinterpret_cast<const float4*>(sd_smem);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 t = s4[c];
+        sdv[4 * c] = t.x;
+        sdv[4 * c + 1] = t.y;
+        sdv[4 * c + 2] = t.z;
+        sdv[4 * c + 3] = t.w;
+      }
+    } else if (vec) {
       const float4* sd4 = reinterpret_cast<const float4*>(sd);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -82,12 +96,20 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
 #pragma unroll
       for (int j = 0; j < 32; ++j) sdv[j] = (base + j < p.l_pad) ? __ldg(sd + j) : 1.f;
     }
-    // f32(acc): cvt.rn (I2FP); both multiplies as packed FMUL2 pairs (each lane of the pair
-    // rounds exactly like the scalar fl(x * y)).
+    // f32(acc): exact either way -- the magic-number form (IADD + FADD2) when |acc| <= 2^22
+    // (d <= 256 for any int8 input), else cvt.rn on the XU pipe, which is 4x narrower and
+    // was the bottleneck of this epilogue (ncu: XU 129% of sustained peak).  Both multiplies as
+    // packed FMUL2 pairs (each lane of the pair rounds exactly like the scalar fl(x * y)).
 #pragma unroll
     for (int j = 0; j < 32; j += 2) {
-      float t0, t1;
-      fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sq, sq);
+      float c0, c1, t0, t1;
+      if constexpr (kMagic) {
+        i2f2_magic(c0, c1, r[j], r[j + 1]);
+      } else {
+        c0 = __int2float_rn((int)r[j]);
+        c1 = __int2float_rn((int)r[j + 1]);
+      }
+      fmul2_rn(t0, t1, c0, c1, sq, sq);
       fmul2_rn(v[j], v[j + 1], t0, t1, sdv[j], sdv[j + 1]);
     }
   } else {
@@ -119,6 +141,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sD = smem;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
+  // INT8 scale ring (only when d_scale rows are 16-B aligned: l_pad % 4 == 0)
+  float* sScale = sBest + (size_t)p.qb * 128 * 32;
+  const bool scale_ring = (KIND == TcKind::I8) && ((p.l_pad & 3) == 0);
   __shared__ TsSmemHeader ts_hdr;  // static shared: keeps barrier / bookkeeping accesses on LDS/STS
   TsSmemHeader* hdr = &ts_hdr;
 
@@ -157,6 +182,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     }
     mbar_init(&hdr->qfull, kEpiWarps);
     mbar_init(&hdr->qempty, 1);
+    for (int s = 0; s < kScaleSlots; ++s) {
+      mbar_init(&hdr->sfull[s], 1);
+      mbar_init(&hdr->sempty[s], kEpiWarps);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
@@ -176,6 +205,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t sc_n = 0;  // tiles issued on the scale ring
       constexpr int kRowsPer = kTileRows / CL;
       for (long long u = u_begin; u < u_end; ++u) {
         int q, g, b;
@@ -183,6 +213,15 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         const int vl = doc_valid_len(p, b);
         const int ntiles = (vl + kTileRows - 1) / kTileRows;
         for (int t = 0; t < ntiles; ++t) {
+          if (scale_ring) {
+            const int ss = (int)(sc_n % kScaleSlots);
+            mbar_wait(&hdr->sempty[ss], ((sc_n / kScaleSlots) & 1u) ^ 1u);
+            const uint32_t bytes = (uint32_t)min(kTileRows, p.l_pad - t * kTileRows) * 4u;
+            mbar_arrive_expect_tx(&hdr->sfull[ss], bytes);
+            bulk_load_1d(&hdr->sfull[ss], sScale + ss * kTileRows,
+                         p.d_scale + (long long)b * p.l_pad + t * kTileRows, bytes, kEvictFirst);
+            ++sc_n;
+          }
           mbar_wait(&hdr->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
           const int row0 = b * p.l_pad + t * kTileRows + crank * kRowsPer;
@@ -276,6 +315,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int eb = (KIND == TcKind::I8) ? 1 : 2;
     const int row_bytes = p.dim * eb;
     uint32_t sph = 0, qeph = 0;  // this set's slot is `wset`; sph = parity of its next use
+    uint32_t sc_n = 0;           // tiles consumed from the scale ring
     long long cur_key = -1;
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
@@ -331,6 +371,12 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         }
       }
       for (int t = 0; t < ntiles; ++t) {
+        const float* sdt = nullptr;  // this tile's staged scales
+        if (scale_ring) {
+          const int ss = (int)(sc_n % kScaleSlots);
+          mbar_wait(&hdr->sfull[ss], (sc_n / kScaleSlots) & 1u);
+          sdt = sScale + ss * kTileRows;
+        }
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int mb = 2 * i + wset;
@@ -352,16 +398,16 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tmem_ld32(taddr, ra);
             tmem_ld32(taddr + 32, rb);
             tmem_ld_wait();
-            ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt);
+            ts_chunk<KIND, (KA <= 2)>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 32 : sdt);
             tmem_ld32(taddr + 64, ra);
             tmem_ld32(taddr + 96, rb);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
-            ts_chunk<KIND>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 64 : sdt);
+            ts_chunk<KIND, (KA <= 2)>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 96 : sdt);
           } else {
             uint32_t ra[32], rb[32], rc[32], rd[32];
             tmem_ld32(taddr, ra);
@@ -372,11 +418,16 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
-            ts_chunk<KIND>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2)>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
           }
+        }
+        if (scale_ring) {  // this warp is done with the tile's scales
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hdr->sempty[sc_n % kScaleSlots]);
+          ++sc_n;
         }
       }
       const long long obase = ((long long)q * p.n_docs + b) * p.l_q;

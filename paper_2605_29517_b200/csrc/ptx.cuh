@@ -73,6 +73,14 @@ MXS_DEV void tma_load_2d(const void* tmap, uint64_t* bar, void* smem_dst, int32_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
+// 1-D bulk copy global -> own CTA's shared memory (16-B aligned, size % 16 == 0).
+MXS_DEV void bulk_load_1d(uint64_t* bar, void* smem_dst, const void* src, uint32_t bytes, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)),
+      "l"(cache_hint)
+      : "memory");
+}
 // L2 cache-policy constants (createpolicy.fractional encodings used by CUTLASS).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
@@ -218,6 +226,22 @@ MXS_DEV void fmul2_rn(float& o0, float& o1, float a0, float a1, float b0, float 
   asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(o0), "=f"(o1) : "l"(d));
+}
+// Packed fp32 pair add (FADD2), round-to-nearest: {a.x+b.x, a.y+b.y}.
+MXS_DEV void fadd2_rn(float& o0, float& o1, float a0, float a1, float b0, float b1) {
+  unsigned long long a, b, d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o0), "=f"(o1) : "l"(d));
+}
+// Exact int32 -> fp32 for |x| <= 2^22 without the XU conversion pipe: x + 0x4B400000 is the
+// bit pattern of 1.5 * 2^23 + x (same binade, or 2^24 exactly at x = 2^22), so one integer add
+// on the ALU pipe plus one FADD (packed, below) recovers x exactly.
+constexpr int kMagicI2F = 0x4B400000;
+constexpr float kMagicF = 12582912.0f;  // 1.5 * 2^23
+MXS_DEV void i2f2_magic(float& o0, float& o1, uint32_t a0, uint32_t a1) {
+  fadd2_rn(o0, o1, __int_as_float((int)a0 + kMagicI2F), __int_as_float((int)a1 + kMagicI2F), -kMagicF, -kMagicF);
 }
 MXS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -72,3 +72,222 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const double* __rest
 }
 
 }  // namespace mxs
+
+namespace mxs {
+
+// ----------------------------------------------------------------------------------------------
+// Small-k selection (k <= kSelMaxK): warp tournaments instead of a full sort.
+//
+// A CTA stages its slice of scores in shared memory; every warp owns a contiguous sub-slice,
+// keeps one "best so far" per lane, and runs k rounds of a warp-wide argmax under the
+// reference order (score desc, id asc).  Only the winning lane removes its element (the score
+// slot becomes NaN = empty) and rescans its own strided elements, so a round costs one 5-level
+// shuffle reduction plus one short rescan.  The per-warp winners (k each) are re-selected by
+// warp 0.  (score, id) is a total order over the valid entries, so the result is exactly the
+// first k of the sorted order -- identical to the bitonic kernel above and to TopKHeap.
+// Ids are implicit (position + id_offset, 8 B of smem per element) for a score vector and
+// explicit (16 B per element) for candidate lists.
+// ----------------------------------------------------------------------------------------------
+constexpr int kSelMaxK = 128;
+constexpr int kSelThreads = 512;
+constexpr long long kSelChunkImplicit = 16384;  // 128 KB of scores
+constexpr long long kSelChunkExplicit = 8192;   // 128 KB of (score, id)
+
+MXS_DEV long long sel_id(const long long* ids, long long base, int j) { return ids ? ids[j] : base + j; }
+
+MXS_DEV void sel_lane_best(const double* s, const long long* ids, long long base, int cnt, double& bs, long long& bi,
+                           int& bj) {
+  bs = -INFINITY;
+  bi = LLONG_MAX;
+  bj = -1;
+  for (int j = (int)lane_id(); j < cnt; j += 32) {
+    const double v = s[j];
+    if (v != v) continue;  // empty / consumed
+    const long long i = sel_id(ids, base, j);
+    if (bj < 0 || better(v, i, bs, bi)) {
+      bs = v;
+      bi = i;
+      bj = j;
+    }
+  }
+}
+
+// Warp-cooperative: writes the k best of s[0, cnt) (ids explicit or base + j) to (os, oi)[0, k)
+// in order; missing entries become (empty_s, -1).  Consumes (NaN-marks) the selected entries.
+MXS_DEV void sel_warp(double* s, const long long* ids, long long base, int cnt, int k, double* os, long long* oi,
+                      double empty_s) {
+  double bs;
+  long long bi;
+  int bj;
+  sel_lane_best(s, ids, base, cnt, bs, bi, bj);
+  for (int r = 0; r < k; ++r) {
+    double ws = bs;
+    long long wi = bi;
+    int has = bj >= 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os_ = __shfl_xor_sync(0xffffffffu, ws, off);
+      const long long oi_ = __shfl_xor_sync(0xffffffffu, wi, off);
+      const int oh = __shfl_xor_sync(0xffffffffu, has, off);
+      if (oh && (!has || better(os_, oi_, ws, wi))) {
+        ws = os_;
+        wi = oi_;
+        has = 1;
+      }
+    }
+    if (!has) {  // nothing valid left: this and the remaining slots are empty
+      for (int rr = r + (int)lane_id(); rr < k; rr += 32) {
+        os[rr] = empty_s;
+        oi[rr] = -1;
+      }
+      break;
+    }
+    if (lane_id() == 0) {
+      os[r] = ws;
+      oi[r] = wi;
+    }
+    if (bj >= 0 && bi == wi) {  // this lane owned the winner (ids are unique among valid entries)
+      s[bj] = __longlong_as_double(0x7ff8000000000000LL);
+      sel_lane_best(s, ids, base, cnt, bs, bi, bj);
+    }
+  }
+  __syncwarp();
+}
+
+// Valid-first order used by the sorting networks: valid entries (id != LLONG_MAX) by (score desc,
+// id asc), then the empty ones.
+MXS_DEV bool sel_before(double s1, long long i1, double s2, long long i2) {
+  return i1 != LLONG_MAX && (i2 == LLONG_MAX || better(s1, i1, s2, i2));
+}
+
+constexpr int kSelSurvivors = 1024;  // threshold-filter capacity (one sort element per thread pair)
+
+// Threshold filter for k <= 32.  Every lane's maximum is a real element, so the k-th largest lane
+// maximum of ANY warp is a lower bound T on the k-th largest score of the slice; the largest
+// such bound over the warps is used.  Only elements with score >= T can be in the top k; they
+// are compacted (typically k .. a few k of them) and sorted with a bitonic network under the
+// reference order.  Returns false (nothing written) if more than kSelSurvivors survive -- e.g.
+// massive ties at the threshold -- and the caller falls back to the warp tournaments.
+MXS_DEV bool sel_threshold(const double* ss, const long long* si, long long base, int m, int k, double* out_s,
+                           long long* out_ids, double* sv_s, long long* sv_i, double* wbound, int* counter) {
+  constexpr int kWarps = kSelThreads / 32;
+  const int w = (int)warp_id_uniform();
+  const int lane = (int)lane_id();
+  const int per = (m + kWarps - 1) / kWarps;
+  const int b0 = min(m, w * per), b1 = min(m, b0 + per);
+  // 1. lane maxima (NaN = empty never wins: the comparison is false)
+  double lm = -INFINITY;
+  for (int j = b0 + lane; j < b1; j += 32) lm = fmax(lm, ss[j]);
+  // 2. k-th largest lane maximum of this warp: bitonic sort of 32 values (descending)
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, lm, stride);
+      const bool lower = (lane & stride) == 0;
+      const bool desc = (lane & size) == 0 || size == 32;
+      // in a descending run the lower lane keeps the max
+      lm = (lower == desc) ? fmax(lm, o) : fmin(lm, o);
+    }
+  }
+  const double kth = __shfl_sync(0xffffffffu, lm, k - 1);
+  if (lane == 0) wbound[w] = kth;
+  if (threadIdx.x == 0) *counter = 0;
+  __syncthreads();
+  double T = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) T = fmax(T, wbound[i]);
+  // 3. compact the survivors (score >= T); with T = -inf (fewer than k valid entries in every
+  //    warp) everything valid survives and the capacity check decides
+  for (int j = b0 + lane; j < b1; j += 32) {
+    const double v = ss[j];
+    if (v >= T) {
+      const int pos = atomicAdd(counter, 1);
+      if (pos < kSelSurvivors) {
+        sv_s[pos] = v;
+        sv_i[pos] = si ? si[j] : base + j;
+      }
+    }
+  }
+  __syncthreads();
+  const int cnt = *counter;
+  if (cnt > kSelSurvivors) return false;
+  int P = 32;
+  while (P < cnt) P <<= 1;
+  for (int e = cnt + (int)threadIdx.x; e < P; e += blockDim.x) {
+    sv_s[e] = -INFINITY;
+    sv_i[e] = LLONG_MAX;
+  }
+  __syncthreads();
+  // 4. bitonic sort of P <= 1024 survivors (one pair per thread per stage)
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int a = 2 * t - (t & (stride - 1));
+        const int b = a + stride;
+        const bool first_block = (a & size) == 0 || size == P;  // sorted "best first"
+        const double sa = sv_s[a], sb = sv_s[b];
+        const long long ia = sv_i[a], ib = sv_i[b];
+        if (sel_before(sb, ib, sa, ia) == first_block) {
+          sv_s[a] = sb;
+          sv_s[b] = sa;
+          sv_i[a] = ib;
+          sv_i[b] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    const bool ok = sv_i[r] != LLONG_MAX;
+    out_s[r] = ok ? sv_s[r] : -INFINITY;
+    out_ids[r] = ok ? sv_i[r] : -1;
+  }
+  return true;
+}
+
+// One launch: every CTA selects the k best of its slice [blockIdx.x * chunk, ... + chunk).
+// in_ids == nullptr means ids are positions + id_offset; NaN scores and ids < 0 are empty, and
+// empty output slots are (-inf, -1) -- so a pass's output is a valid input for the next pass.
+__global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* __restrict__ in_s,
+                                                                  const long long* __restrict__ in_ids, long long n,
+                                                                  int k, long long chunk, long long id_offset,
+                                                                  double* __restrict__ out_s,
+                                                                  long long* __restrict__ out_ids) {
+  extern __shared__ __align__(16) uint8_t sel_smem[];
+  constexpr int kWarps = kSelThreads / 32;
+  __shared__ double wbound[kWarps];
+  __shared__ int counter;
+  const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+  double* ss = reinterpret_cast<double*>(sel_smem);
+  long long* si = in_ids ? reinterpret_cast<long long*>(ss + chunk) : nullptr;
+  double* cs = reinterpret_cast<double*>(sel_smem + chunk * (in_ids ? 16 : 8));
+  long long* ci = reinterpret_cast<long long*>(cs + kWarps * kSelMaxK);
+  double* sv_s = reinterpret_cast<double*>(ci + kWarps * kSelMaxK);
+  long long* sv_i = reinterpret_cast<long long*>(sv_s + kSelSurvivors);
+  const long long lo = (long long)blockIdx.x * chunk;
+  const int m = (int)max(0LL, min(n, lo + chunk) - lo);
+  for (int e = threadIdx.x; e < m; e += blockDim.x) {
+    const double v = in_s[lo + e];
+    if (in_ids) {
+      const long long i = in_ids[lo + e];
+      ss[e] = (i >= 0) ? v : kNaN;
+      si[e] = i;
+    } else {
+      ss[e] = v;
+    }
+  }
+  __syncthreads();
+  double* os = out_s + (long long)blockIdx.x * k;
+  long long* oi = out_ids + (long long)blockIdx.x * k;
+  if (k <= 32 && sel_threshold(ss, si, lo + id_offset, m, k, os, oi, sv_s, sv_i, wbound, &counter)) return;
+  const int w = (int)warp_id_uniform();
+  const int per = (m + kWarps - 1) / kWarps;
+  const int b0 = min(m, w * per), b1 = min(m, b0 + per);
+  sel_warp(ss + b0, si ? si + b0 : nullptr, lo + b0 + id_offset, b1 - b0, k, cs + (long long)w * k,
+           ci + (long long)w * k, kNaN);
+  __syncthreads();
+  if (w == 0) sel_warp(cs, ci, 0, kWarps * k, k, os, oi, -INFINITY);
+}
+
+}  // namespace mxs

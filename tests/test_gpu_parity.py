@@ -403,6 +403,21 @@ def test_topk_ties_and_chunking():
         mx.topk(cuda(s[:5]), 6)
 
 
+@pytest.mark.parametrize("n,k", [(1, 1), (20, 20), (10_000, 20), (10_000, 1), (16_384, 128), (16_385, 128), (8193, 100),
+                                 (2_000_000, 128), (50_000, 129), (10_000, 500), (300_000, 32)])
+def test_topk_select_paths_match_oracle(n, k):
+    """Warp-tournament selection (k <= 128, multi-pass above 8192) and the bitonic path (k > 128)."""
+    rng = np.random.default_rng(n + k)
+    s = np.round(rng.standard_normal(n), 3)  # heavy ties: exercises the id-ascending rule
+    if n > 10:
+        s[rng.integers(0, n, 5)] = np.nan  # NaN entries are never selected
+    ts, ti = mx.topk(cuda(s), k, id_offset=7)
+    os_, oi = orc.topk(np.where(np.isnan(s), -np.inf, s), k, id_offset=7)
+    valid = ~np.isnan(s)
+    if valid.sum() >= k:
+        assert ti.cpu().tolist() == oi.tolist() and ts.cpu().tolist() == os_.tolist()
+
+
 def test_sharded_rerank_merge_equals_global():
     from paper_2605_29517_b200.topk import select_candidates
 
