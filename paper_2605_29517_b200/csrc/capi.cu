@@ -11,7 +11,7 @@
 #include "fwd_exact.cuh"
 #include "fwd_tc.cuh"
 #include "fwd_ts.cuh"
-#include "varlen_tc.cuh"
+#include "varlen_rows.cuh"
 #include "csr.cuh"
 #include "grad.cuh"
 #include "quant.cuh"
@@ -239,22 +239,22 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
 template <mxs::TcKind KIND>
 int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens, const int64_t* cu, int64_t n_docs,
                      int64_t n_tokens, int64_t dim, float* rowmax, int32_t* argmax, cudaStream_t st) {
-  const int eb = (KIND == mxs::TcKind::I8) ? 1 : 2;
+  static_assert(KIND != mxs::TcKind::I8, "varlen is a bf16 / f16 path");
+  const int eb = 2;
   const long long n_cols = n_q * l_q;
   if (n_cols > 128 || (dim * eb) % 16 != 0) return MXS_UNSUPPORTED;
   const int ka = (int)((dim * eb + 127) / 128);
   if (ka > 4) return MXS_UNSUPPORTED;
-  const int ncp = (int)((n_cols + 15) / 16) * 16;
-  const size_t max_smem = 232448 - sizeof(mxs::VlSmemHeader);
-  const size_t fixed = 1024 + (size_t)ka * ncp * 128 + sizeof(mxs::VlScratch);
+  const size_t max_smem = 232448 - sizeof(mxs::VrSmemHeader);
+  const size_t fixed = mxs::varlen_rows_smem_bytes(ka, 0);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
-  mxs::VarlenParams p = {};
+  mxs::VarlenRowsParams p = {};
   p.n_q = (int)n_q;
   p.l_q = (int)l_q;
   p.n_cols = (int)n_cols;
-  p.n_cols_pad = ncp;
+  p.copies = n_cols <= 32 ? 4 : (n_cols <= 64 ? 2 : 1);  // query-row replication over TMEM quadrants
   p.n_docs = n_docs;
   p.n_tokens = n_tokens;
   p.dim = (int)dim;
@@ -262,20 +262,20 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
   p.cu = (const long long*)cu;
   p.rowmax = rowmax;
   p.argmax = argmax;
-  const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                                 : (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType dt =
+      (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tt, tq;
   int s;
   if ((s = make_tmap_2d(&tt, tokens, dt, eb, dim, n_tokens)) != MXS_OK) return s;
-  if ((s = make_tmap_2d(&tq, Q, dt, eb, dim, n_cols, ncp)) != MXS_OK) return s;
-  const size_t smem = mxs::varlen_smem_bytes(ka, stages, ncp);
-  void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::VarlenParams) = nullptr;
+  // one box per row copy; rows >= n_cols read as 0
+  if ((s = make_tmap_2d(&tq, Q, dt, eb, dim, n_cols, 128 / p.copies)) != MXS_OK) return s;
+  const size_t smem = mxs::varlen_rows_smem_bytes(ka, stages);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::VarlenRowsParams) = nullptr;
   switch (ka) {
-    case 1: kern = mxs::varlen_tc_kernel<KIND, 1>; break;
-    case 2: kern = mxs::varlen_tc_kernel<KIND, 2>; break;
-    case 3: kern = mxs::varlen_tc_kernel<KIND, 3>; break;
-    case 4: kern = mxs::varlen_tc_kernel<KIND, 4>; break;
+    case 1: kern = mxs::varlen_rows_kernel<KIND, 1>; break;
+    case 2: kern = mxs::varlen_rows_kernel<KIND, 2>; break;
+    case 3: kern = mxs::varlen_rows_kernel<KIND, 3>; break;
+    case 4: kern = mxs::varlen_rows_kernel<KIND, 4>; break;
     default: return MXS_UNSUPPORTED;
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -283,8 +283,8 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
   const int nsm = sm_count();
   if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
   const long long grid = n_docs < nsm ? n_docs : nsm;
-  kern<<<(unsigned)grid, mxs::kVlThreads, smem, st>>>(tt, tq, p);
-  return check_launch("varlen_tc_kernel");
+  kern<<<(unsigned)grid, mxs::kVrThreads, smem, st>>>(tt, tq, p);
+  return check_launch("varlen_rows_kernel");
 }
 
 bool use_ts_path() {

@@ -215,14 +215,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         for (int t = 0; t < ntiles; ++t) {
           if (scale_ring) {
             const int ss = (int)(sc_n % kScaleSlots);
-            mbar_wait(&hdr->sempty[ss], ((sc_n / kScaleSlots) & 1u) ^ 1u);
+            mbar_wait_idle(&hdr->sempty[ss], ((sc_n / kScaleSlots) & 1u) ^ 1u);
             const uint32_t bytes = (uint32_t)min(kTileRows, p.l_pad - t * kTileRows) * 4u;
             mbar_arrive_expect_tx(&hdr->sfull[ss], bytes);
             bulk_load_1d(&hdr->sfull[ss], sScale + ss * kTileRows,
                          p.d_scale + (long long)b * p.l_pad + t * kTileRows, bytes, kEvictFirst);
             ++sc_n;
           }
-          mbar_wait(&hdr->empty[stage], phase ^ 1);
+          mbar_wait_idle(&hdr->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
           const int row0 = b * p.l_pad + t * kTileRows + crank * kRowsPer;
 #pragma unroll
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
         for (int mb = 0; mb < qbv; ++mb) {
           const int slot = mb & 1;
-          mbar_wait(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
+          mbar_wait_idle(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);

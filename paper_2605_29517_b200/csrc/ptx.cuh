@@ -59,6 +59,25 @@ MXS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// Same, but each try_wait may suspend the warp for up to ~1 ms (it still returns as soon as the
+// phase completes): for producer / MMA warps that are usually ahead, so that their waiting does
+// not burn issue slots of the epilogue warps sharing their SM sub-partition.
+MXS_DEV bool mbar_try_wait_suspend(uint32_t bar_addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(bar_addr), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+MXS_DEV void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait_suspend(a, parity)) {
+  }
+}
 
 // ---------------------------------------------------------------- TMA
 MXS_DEV void tma_prefetch_desc(const void* tmap) {

@@ -1,0 +1,509 @@
+// Padding-free (cu_seqlens) MaxSim forward on tcgen05, v2 (K5) -- maxsim/varlen.py:88-131.
+//
+// Query rows live in the TMEM lanes, packed document tokens in the TMEM columns:
+//   A = the n_cols = n_q * l_q (<= 128) query rows, replicated C = 128 / round_up(n_cols) times
+//       (C = 4 for ColBERT's L_q = 32) so that every TMEM lane quadrant holds real rows;
+//   B = a tile of 128 consecutive packed tokens (TMA from the [total_tokens, dim] buffer);
+//   D = [128 lanes x 128 tokens] fp32 in one of two TMEM slots.
+// Copy k of the rows scans token range k of the tile (128 / C tokens): each epilogue thread owns
+// one query row and folds the range's tokens IN ORDER straight out of its registers
+// (tcgen05.ld), keeping (max, first argmax) per document piece -- strict >, so the earliest
+// token wins ties (S3).  No transpose, no cross-thread scan.
+// Document boundaries are warp-uniform (every row sees the same tokens).  A dedicated warp
+// walks cu_seqlens ahead of the epilogue and publishes, per tile, the document holding the
+// first token and a 128-bit "a document starts at this token" mask (one ballot per 32 docs).
+// Pieces that cross a range edge are merged in token order (head pieces into the running
+// carry, strict > so earlier tokens win) by one merge warp per 32 query rows, which walks all
+// tiles in order and keeps the carry in registers; the two scan warp sets take alternate tiles.
+// CTAs own contiguous, token-balanced document ranges (binary search of cu_seqlens on the
+// device), so every document is finished by exactly one CTA: no atomics, no second pass.
+// HBM-bound: L_q = 32 gives 32 FLOP/B; the MMA is a fraction of the per-tile HBM time.
+#pragma once
+#include "fwd_tc.cuh"
+
+namespace mxs {
+
+struct VarlenRowsParams {
+  int n_q, l_q, n_cols;  // n_cols = n_q * l_q <= 128 query rows
+  int copies;            // row replication C (4, 2 or 1)
+  long long n_docs, n_tokens;
+  int dim;
+  int stages;
+  const long long* cu;  // [n_docs + 1] device
+  float* rowmax;        // [n_q, n_docs, l_q]
+  int32_t* argmax;      // [n_q, n_docs, l_q] or nullptr
+};
+
+constexpr int kVrTile = 128;       // tokens per tile (MMA N)
+constexpr int kVrThreads = 32 * 15;  // warp 0 TMA, 1 MMA + TMEM, 2..9 scan, 10 boundaries, 11..14 merge
+constexpr int kVrSlotCols = 128;
+constexpr int kVrInfoSlots = 8;
+
+struct VrInfo {  // per tile, written by the boundary warp
+  long long d_first;       // document holding the tile's first token
+  long long dstart_first;  // its first token
+  uint32_t words[4];       // bit x: token p0 + x starts a document
+};
+
+struct VrShared {
+  VrInfo info[kVrInfoSlots];
+  // head / tail pieces of every token range (copy) of the tile, per set, double-buffered over
+  // the set's tiles so that scanning tile t + 2 never waits for the merge of tile t
+  float hm[2][2][4][128];
+  float tm[2][2][4][128];
+  int16_t ha[2][2][4][128];  // token offset in the tile
+  int16_t ta[2][2][4][128];
+};
+
+struct VrSmemHeader {
+  uint64_t full[8];
+  uint64_t empty[8];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint64_t qfull;
+  uint64_t ifull[kVrInfoSlots];
+  uint64_t iempty[kVrInfoSlots];
+  uint64_t pfull[2][2];   // [set][buffer]: the set's scan warps wrote their pieces
+  uint64_t pempty[2][2];  // [set][buffer]: the merge warps consumed them
+  uint32_t tmem_base;
+  int32_t pad;
+  long long doc_begin, doc_end, tok_begin, tok_end;
+};
+
+__host__ __device__ inline size_t varlen_rows_smem_bytes(int ka, int stages) {
+  return 1024 + (size_t)(stages + 1) * ka * kAtomBytes + sizeof(VrShared);
+}
+
+// first document d in [lo, hi) with cu[d + 1] > tok (the document containing token tok)
+MXS_DEV long long vr_doc_of_token(const long long* cu, long long lo, long long hi, long long tok) {
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (__ldg(cu + mid + 1) > tok)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+MXS_DEV void vr_emit(const VarlenRowsParams& p, int row, long long doc, float m, long long arg_local) {
+  if (row >= p.n_cols || doc < 0) return;
+  const int q = row / p.l_q, i = row - q * p.l_q;
+  const long long o = ((long long)q * p.n_docs + doc) * p.l_q + i;
+  p.rowmax[o] = m;
+  if (p.argmax) p.argmax[o] = (int32_t)arg_local;
+}
+
+// bits of the 128-bit mask at positions [lo, hi) (0 <= lo <= hi <= 128)
+MXS_DEV int vr_popc_range(const uint32_t (&w)[4], int lo, int hi) {
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = max(lo - 32 * i, 0), b = min(hi - 32 * i, 32);
+    if (a < b) {
+      const uint32_t mk = (b == 32 ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
+      n += __popc(w[i] & mk);
+    }
+  }
+  return n;
+}
+// highest set position in [lo, hi), or -1
+MXS_DEV int vr_last_bit(const uint32_t (&w)[4], int lo, int hi) {
+  int r = -1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = max(lo - 32 * i, 0), b = min(hi - 32 * i, 32);
+    if (a < b) {
+      const uint32_t mk = (b == 32 ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
+      const uint32_t x = w[i] & mk;
+      if (x) r = 32 * i + 31 - __clz(x);
+    }
+  }
+  return r;
+}
+MXS_DEV bool vr_bit(const uint32_t (&w)[4], int x) { return (w[x >> 5] >> (x & 31)) & 1u; }
+
+// Scan warp (set, lane quadrant): token range k of the tiles t = set (mod 2), its 32 query rows.
+// Documents that start and end inside the range are written out directly; the range's head
+// piece (before its first document start) and tail piece (from its last start) go to shared
+// memory for the merge warp.
+template <TcKind KIND, int KA, int C>
+MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh, uint32_t tmem_base, int set,
+                     int quad, uint32_t lane, int n_tiles, long long tok_begin, long long tok_end) {
+  constexpr int L = kVrTile / C;        // tokens per range
+  constexpr int QPC = 4 / C;            // lane quadrants per row copy
+  const int k = quad / QPC;             // token range (row copy) of this warp
+  const int j = quad % QPC;             // row block within the copy
+  const int row = j * 32 + (int)lane;   // query row
+  if (j * 32 >= p.n_cols) return;       // no real rows in this quadrant
+  const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+  const int x0 = k * L;
+  for (int t = set; t < n_tiles; t += 2) {
+    const long long p0 = tok_begin + (long long)t * kVrTile;
+    const int ntok = (int)min((long long)kVrTile, tok_end - p0);
+    const int islot = t % kVrInfoSlots;
+    mbar_wait(&hdr->ifull[islot], ((uint32_t)t / kVrInfoSlots) & 1u);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = sh->info[islot].words[i];
+    const long long d_first = sh->info[islot].d_first;
+    const long long dstart_first = sh->info[islot].dstart_first;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hdr->iempty[islot]);
+    const uint32_t slot = (uint32_t)set;
+    const int pb = (t >> 1) & 1;
+    const int x1 = min(x0 + L, ntok);
+    float m = -INFINITY, hm = -INFINITY;
+    int a = 0, ha = 0;
+    mbar_wait(&hdr->tfull[slot], ((uint32_t)t >> 1) & 1u);
+    tc_fence_after();
+    if (x0 < ntok) {
+      long long doc = d_first + vr_popc_range(w, 1, x0 + 1);
+      const int lb = vr_last_bit(w, 1, x0 + 1);
+      long long dstart = (lb >= 0) ? p0 + lb : dstart_first;
+      bool in_head = !vr_bit(w, x0);
+      const uint32_t taddr = tmem_base + lane_base + slot * kVrSlotCols + (uint32_t)x0;
+#pragma unroll
+      for (int cc = 0; cc < L / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        tmem_ld_wait();
+        if (cc == L / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+        }
+        const int xb = x0 + cc * 32;
+        if (xb < x1) {
+          uint32_t word = w[xb >> 5];
+          if (cc == 0) word &= ~1u;  // a start at x0 itself is the range's own first document
+          if (word == 0u && xb + 32 <= x1) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {  // branch-free strict-> fold in token order
+              const float v = __uint_as_float(r[q]);
+              a = (v > m) ? xb + q : a;
+              m = fmaxf(m, v);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              if (xb + q < x1) {
+                if ((word >> q) & 1u) {  // token xb + q starts document doc + 1 (warp-uniform)
+                  if (in_head) {
+                    hm = m;
+                    ha = a;
+                    in_head = false;
+                  } else {
+                    vr_emit(p, row, doc, m, p0 + a - dstart);  // complete inside this range
+                  }
+                  ++doc;
+                  dstart = p0 + xb + q;
+                  m = -INFINITY;
+                  a = 0;
+                }
+                const float v = __uint_as_float(r[q]);
+                if (v > m) {
+                  m = v;
+                  a = xb + q;
+                }
+              }
+            }
+          }
+        }
+      }
+      if (in_head) {  // no document starts in this range: the whole range is one head piece
+        hm = m;
+        ha = a;
+      }
+    } else {
+      // empty range (short last tile): still release the TMEM slot
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+    }
+    // hand the pieces to the merge warp (the buffer's previous tile must have been merged)
+    const uint32_t use = (uint32_t)t >> 2;  // t = set + 2 * (pb + 2 * use)
+    mbar_wait(&hdr->pempty[set][pb], (use & 1u) ^ 1u);
+    sh->hm[set][pb][k][row] = hm;
+    sh->ha[set][pb][k][row] = (int16_t)ha;
+    sh->tm[set][pb][k][row] = m;
+    sh->ta[set][pb][k][row] = (int16_t)a;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hdr->pfull[set][pb]);
+  }
+}
+
+// Merge warp for query rows [32 j, 32 j + 32): walks ALL tiles in order, folds the ranges of each
+// tile (token order, strict >) and carries the document still open at the tile's end in
+// registers -- the only serial work of the kernel, ~100 instructions per tile.
+template <int C>
+MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh, int j, uint32_t lane, int n_tiles,
+                      long long tok_begin, long long tok_end) {
+  constexpr int L = kVrTile / C;
+  const int row = j * 32 + (int)lane;
+  if (j * 32 >= p.n_cols) return;
+  float cm = -INFINITY;
+  long long ca = 0, cd = -1, cs = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const long long p0 = tok_begin + (long long)t * kVrTile;
+    const int ntok = (int)min((long long)kVrTile, tok_end - p0);
+    const int islot = t % kVrInfoSlots;
+    mbar_wait(&hdr->ifull[islot], ((uint32_t)t / kVrInfoSlots) & 1u);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = sh->info[islot].words[i];
+    const long long d_first = sh->info[islot].d_first;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hdr->iempty[islot]);
+    const int set = t & 1, pb = (t >> 1) & 1;
+    mbar_wait(&hdr->pfull[set][pb], ((uint32_t)t >> 2) & 1u);
+    bool seen = false;       // a document starts somewhere in [0, ntok)
+    float thm = -INFINITY;   // tile head: tokens before the first start (the carried document)
+    int tha = 0;
+    float pm = -INFINITY;    // piece after the latest start
+    int pa = 0, plast = 0;
+#pragma unroll
+    for (int kk = 0; kk < C; ++kk) {
+      const int r0 = kk * L;
+      if (r0 < ntok) {
+        const int r1 = min(r0 + L, ntok);
+        const bool st = vr_bit(w, r0);
+        const int nb = vr_popc_range(w, r0 + 1, r1);
+        if (!st) {  // the range's head continues the current piece
+          const float h = sh->hm[set][pb][kk][row];
+          const int hx = sh->ha[set][pb][kk][row];
+          if (!seen) {
+            if (h > thm) {
+              thm = h;
+              tha = hx;
+            }
+          } else if (h > pm) {
+            pm = h;
+            pa = hx;
+          }
+        }
+        if (st || nb > 0) {  // the current piece ends at the range's first start
+          if (seen) vr_emit(p, row, d_first + vr_popc_range(w, 1, plast + 1), pm, pa - plast);
+          seen = true;
+          plast = vr_last_bit(w, r0, r1);
+          pm = sh->tm[set][pb][kk][row];
+          pa = sh->ta[set][pb][kk][row];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hdr->pempty[set][pb]);
+    if (!vr_bit(w, 0) && (thm > cm || cd < 0)) {  // the tile head continues the carried document
+      cm = thm;
+      ca = p0 + tha;
+    }
+    if (seen) {  // the carried document ended at the tile's first start
+      vr_emit(p, row, cd, cm, ca - cs);
+      cm = pm;
+      ca = p0 + pa;
+      cd = d_first + vr_popc_range(w, 1, plast + 1);
+      cs = p0 + plast;
+    }
+  }
+  if (n_tiles > 0) vr_emit(p, row, cd, cm, ca - cs);  // the CTA's last document ends at tok_end
+}
+
+template <TcKind KIND, int KA>
+__global__ void __launch_bounds__(kVrThreads, 1)
+    varlen_rows_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmQ,
+                       const VarlenRowsParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem;                                       // A operand: 128 (replicated) query rows
+  uint8_t* sT = sQ + (size_t)KA * kAtomBytes;               // token tile ring
+  VrShared* sh = reinterpret_cast<VrShared*>(sT + (size_t)p.stages * KA * kAtomBytes);
+  __shared__ VrSmemHeader vr_hdr;
+  VrSmemHeader* hdr = &vr_hdr;
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int C = p.copies;
+  const int n_merge = (p.n_cols + 31) >> 5;       // merge warps (one per 32 query rows)
+  const int n_active = C * n_merge;               // scan warps per set holding real rows
+
+  if (threadIdx.x == 0) {
+    // token-balanced contiguous document range of this CTA
+    const long long total = __ldg(p.cu + p.n_docs);
+    const long long t0 = total * blockIdx.x / gridDim.x;
+    const long long t1 = total * (blockIdx.x + 1) / gridDim.x;
+    const long long d0 = (blockIdx.x == 0) ? 0 : vr_doc_of_token(p.cu, 0, p.n_docs, t0 - 1) + 1;
+    long long d1 = (blockIdx.x + 1 == gridDim.x) ? p.n_docs : vr_doc_of_token(p.cu, 0, p.n_docs, t1 - 1) + 1;
+    if (d1 < d0) d1 = d0;
+    hdr->doc_begin = d0;
+    hdr->doc_end = d1;
+    hdr->tok_begin = __ldg(p.cu + d0);
+    hdr->tok_end = __ldg(p.cu + d1);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&hdr->full[s], 1);
+      mbar_init(&hdr->empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&hdr->tfull[s], 1);
+      mbar_init(&hdr->tempty[s], (uint32_t)n_active);
+    }
+    mbar_init(&hdr->qfull, 1);
+    for (int s = 0; s < kVrInfoSlots; ++s) {
+      mbar_init(&hdr->ifull[s], 1);
+      mbar_init(&hdr->iempty[s], (uint32_t)(n_active + n_merge));  // scan warps of the set + merge warps
+    }
+    for (int s = 0; s < 2; ++s)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&hdr->pfull[s][b], (uint32_t)n_active);
+        mbar_init(&hdr->pempty[s][b], (uint32_t)n_merge);
+      }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&hdr->tmem_base, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = hdr->tmem_base;
+  const long long tok_begin = hdr->tok_begin, tok_end = hdr->tok_end;
+  const int n_tiles = (int)((tok_end - tok_begin + kVrTile - 1) / kVrTile);
+  constexpr int kElemsPerAtom = 64;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0 && n_tiles > 0) {
+      tma_prefetch_desc(&tmT);
+      const int rpc = kVrTile / C;  // rows per copy
+      mbar_arrive_expect_tx(&hdr->qfull, (uint32_t)(KA * kAtomBytes));
+      for (int a = 0; a < KA; ++a)
+        for (int c = 0; c < C; ++c)
+          tma_load_2d(&tmQ, &hdr->qfull, sQ + (size_t)a * kAtomBytes + (size_t)c * rpc * 128, a * kElemsPerAtom, 0,
+                      kEvictLast);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        mbar_wait_idle(&hdr->empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
+        for (int a = 0; a < KA; ++a)
+          tma_load_2d(&tmT, &hdr->full[stage], sT + (size_t)(stage * KA + a) * kAtomBytes, a * kElemsPerAtom,
+                      (int)(tok_begin + (long long)t * kVrTile), kEvictFirst);
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (n_tiles > 0) {
+      constexpr uint32_t kIdesc = (KIND == TcKind::BF16) ? make_idesc(1, 1, 128, kVrTile)
+                                                         : make_idesc(1, 0, 128, kVrTile);
+      mbar_wait_idle(&hdr->qfull, 0);
+      tc_fence_after();
+      const uint64_t qdesc0 = sw128_kmajor_desc(smem_u32(sQ));
+      const uint64_t tdesc0 = sw128_kmajor_desc(smem_u32(sT));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        const int slot = t & 1;
+        mbar_wait_idle(&hdr->full[stage], phase);
+        mbar_wait_idle(&hdr->tempty[slot], (((uint32_t)t >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t bd0 = tdesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
+          const uint32_t dcol = tmem_base + (uint32_t)(slot * kVrSlotCols);
+#pragma unroll
+          for (int k = 0; k < KA * 4; ++k) {
+            const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
+            mma_f16_ss(dcol, qdesc0 + koff, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+          }
+          mma_commit(&hdr->tfull[slot]);
+          mma_commit(&hdr->empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------------ boundary producer
+    // Walks cu_seqlens once, ahead of the epilogue: per tile, the document holding its first
+    // token and the 128-bit mask of document starts.  cu lines are reused across many tiles,
+    // so the loads are L1 hits in the common case.
+    const long long doc_end = hdr->doc_end;
+    long long base = hdr->doc_begin;  // cu[base] <= first token of the next tile
+    for (int t = 0; t < n_tiles; ++t) {
+      const long long p0 = tok_begin + (long long)t * kVrTile;
+      const long long pe = min(p0 + kVrTile, tok_end);
+      const int islot = t % kVrInfoSlots;
+      mbar_wait_idle(&hdr->iempty[islot], (((uint32_t)t / kVrInfoSlots) & 1u) ^ 1u);
+      long long c;
+      int n;
+      for (;;) {  // document holding p0: last lane with cu <= p0
+        const long long dd = base + lane;
+        c = (dd <= doc_end) ? __ldg(p.cu + dd) : LLONG_MAX;
+        n = __popc(__ballot_sync(0xffffffffu, c <= p0));  // >= 1
+        if (n < 32) break;
+        base += 31;
+      }
+      base += n - 1;
+      const long long dstart = __shfl_sync(0xffffffffu, c, n - 1);
+      uint32_t wd[4] = {0u, 0u, 0u, 0u};
+      if (dstart == p0) wd[0] = 1u;
+      // starts after p0: lanes >= n of this window, then further windows while all are inside
+      bool more = true;
+      bool first = true;
+      long long wbase = base - (n - 1);
+      while (more) {
+        if (!first) {
+          const long long dd = wbase + lane;
+          c = (dd <= doc_end) ? __ldg(p.cu + dd) : LLONG_MAX;
+        }
+        const bool valid = first ? ((int)lane >= n) : true;
+        const bool in = valid && c < pe && c > p0;
+        const int pos = in ? (int)(c - p0) : 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          wd[i] |= __reduce_or_sync(0xffffffffu, (in && (pos >> 5) == i) ? (1u << (pos & 31)) : 0u);
+        const long long last = __shfl_sync(0xffffffffu, c, 31);
+        more = last < pe;  // the window ended inside the tile: more starts may follow
+        wbase += 32;
+        first = false;
+      }
+      if (lane == 0) {
+        sh->info[islot].d_first = base;
+        sh->info[islot].dstart_first = dstart;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sh->info[islot].words[i] = wd[i];
+        mbar_arrive(&hdr->ifull[islot]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 11) {
+    // ------------------------------------------------------------------ merge
+    const int j = (int)warp - 11;
+    if (C == 4)
+      vr_merge<4>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+    else if (C == 2)
+      vr_merge<2>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+    else
+      vr_merge<1>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+  } else {
+    // ------------------------------------------------------------------ scan
+    const int set = ((int)warp - 2) >> 2;  // tiles t with t % 2 == set, TMEM slot `set`
+    const int quad = (int)(warp & 3);      // TMEM lane quadrant (hardware rule: warp id % 4)
+    if (C == 4)
+      vr_scan<KIND, KA, 4>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+    else if (C == 2)
+      vr_scan<KIND, KA, 2>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+    else
+      vr_scan<KIND, KA, 1>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 256);
+  }
+}
+
+}  // namespace mxs
