@@ -37,7 +37,8 @@ struct VarlenRowsParams {
 constexpr int kVrTile = 128;       // tokens per tile (MMA N)
 constexpr int kVrThreads = 32 * 15;  // warp 0 TMA, 1 MMA + TMEM, 2..9 scan, 10 boundaries, 11..14 merge
 constexpr int kVrSlotCols = 128;
-constexpr int kVrInfoSlots = 8;
+constexpr int kVrInfoSlots = 16;
+constexpr int kVrPieceBufs = 4;
 
 struct VrInfo {  // per tile, written by the boundary warp
   long long d_first;       // document holding the tile's first token
@@ -47,12 +48,12 @@ struct VrInfo {  // per tile, written by the boundary warp
 
 struct VrShared {
   VrInfo info[kVrInfoSlots];
-  // head / tail pieces of every token range (copy) of the tile, per set, double-buffered over
-  // the set's tiles so that scanning tile t + 2 never waits for the merge of tile t
-  float hm[2][2][4][128];
-  float tm[2][2][4][128];
-  int16_t ha[2][2][4][128];  // token offset in the tile
-  int16_t ta[2][2][4][128];
+  // head / tail pieces of every (token range k, query row) of a tile at [k * 128 / C + row],
+  // per set, in a ring of kVrPieceBufs buffers so that the scan runs ahead of the merge
+  float hm[2][kVrPieceBufs][128];
+  float tm[2][kVrPieceBufs][128];
+  int16_t ha[2][kVrPieceBufs][128];  // token offset in the tile
+  int16_t ta[2][kVrPieceBufs][128];
 };
 
 struct VrSmemHeader {
@@ -63,8 +64,8 @@ struct VrSmemHeader {
   uint64_t qfull;
   uint64_t ifull[kVrInfoSlots];
   uint64_t iempty[kVrInfoSlots];
-  uint64_t pfull[2][2];   // [set][buffer]: the set's scan warps wrote their pieces
-  uint64_t pempty[2][2];  // [set][buffer]: the merge warps consumed them
+  uint64_t pfull[2][kVrPieceBufs];   // [set][buffer]: the set's scan warps wrote their pieces
+  uint64_t pempty[2][kVrPieceBufs];  // [set][buffer]: the merge warps consumed them
   uint32_t tmem_base;
   int32_t pad;
   long long doc_begin, doc_end, tok_begin, tok_end;
@@ -86,10 +87,15 @@ MXS_DEV long long vr_doc_of_token(const long long* cu, long long lo, long long h
   return lo;
 }
 
-MXS_DEV void vr_emit(const VarlenRowsParams& p, int row, long long doc, float m, long long arg_local) {
-  if (row >= p.n_cols || doc < 0) return;
+// output offset of (query row, document 0); rows >= n_cols get -1 (nothing is written)
+MXS_DEV long long vr_row_base(const VarlenRowsParams& p, int row) {
+  if (row >= p.n_cols) return -1;
   const int q = row / p.l_q, i = row - q * p.l_q;
-  const long long o = ((long long)q * p.n_docs + doc) * p.l_q + i;
+  return (long long)q * p.n_docs * p.l_q + i;
+}
+MXS_DEV void vr_emit(const VarlenRowsParams& p, long long rbase, long long doc, float m, long long arg_local) {
+  if (rbase < 0 || doc < 0) return;
+  const long long o = rbase + doc * p.l_q;
   p.rowmax[o] = m;
   if (p.argmax) p.argmax[o] = (int32_t)arg_local;
 }
@@ -136,6 +142,8 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
   const int j = quad % QPC;             // row block within the copy
   const int row = j * 32 + (int)lane;   // query row
   if (j * 32 >= p.n_cols) return;       // no real rows in this quadrant
+  const long long rbase = vr_row_base(p, row);
+  const int pidx = k * (kVrTile / C) + row;  // piece slot of (range k, row)
   const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
   const int x0 = k * L;
   for (int t = set; t < n_tiles; t += 2) {
@@ -151,7 +159,7 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->iempty[islot]);
     const uint32_t slot = (uint32_t)set;
-    const int pb = (t >> 1) & 1;
+    const int pb = (t >> 1) % kVrPieceBufs;
     const int x1 = min(x0 + L, ntok);
     float m = -INFINITY, hm = -INFINITY;
     int a = 0, ha = 0;
@@ -194,7 +202,7 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
                     ha = a;
                     in_head = false;
                   } else {
-                    vr_emit(p, row, doc, m, p0 + a - dstart);  // complete inside this range
+                    vr_emit(p, rbase, doc, m, p0 + a - dstart);  // complete inside this range
                   }
                   ++doc;
                   dstart = p0 + xb + q;
@@ -222,14 +230,68 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
       if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
     }
     // hand the pieces to the merge warp (the buffer's previous tile must have been merged)
-    const uint32_t use = (uint32_t)t >> 2;  // t = set + 2 * (pb + 2 * use)
+    const uint32_t use = ((uint32_t)t >> 1) / kVrPieceBufs;  // t = set + 2 * (pb + kVrPieceBufs * use)
     mbar_wait(&hdr->pempty[set][pb], (use & 1u) ^ 1u);
-    sh->hm[set][pb][k][row] = hm;
-    sh->ha[set][pb][k][row] = (int16_t)ha;
-    sh->tm[set][pb][k][row] = m;
-    sh->ta[set][pb][k][row] = (int16_t)a;
+    sh->hm[set][pb][pidx] = hm;
+    sh->ha[set][pb][pidx] = (int16_t)ha;
+    sh->tm[set][pb][pidx] = m;
+    sh->ta[set][pb][pidx] = (int16_t)a;
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->pfull[set][pb]);
+  }
+}
+
+// Fold the C token ranges of one tile for one query row, in token order, without the carry:
+// the tile head (tokens before the tile's first document start) and the piece after its last
+// start are returned; documents lying between two starts are written out here.
+struct VrTileFold {
+  bool seen = false;        // a document starts somewhere in the tile
+  float thm = -INFINITY;    // tile head
+  int tha = 0;
+  float pm = -INFINITY;     // piece after the latest start
+  int pa = 0, plast = 0;    // its max position and its start (tile offsets)
+  long long pd = 0;         // its document
+};
+template <int C, bool FULL>
+MXS_DEV void vr_fold_ranges(VrTileFold& f, const float* hm, const int16_t* ha, const float* tm, const int16_t* ta,
+                            const uint32_t (&w)[4], long long d_first, int ntok, int row, const VarlenRowsParams& p,
+                            long long rbase) {
+  constexpr int L = kVrTile / C;
+  float h[C], tl[C];
+  int hx[C], tx[C];
+#pragma unroll
+  for (int kk = 0; kk < C; ++kk) {  // all loads first (independent LDS)
+    h[kk] = hm[kk * L + row];
+    hx[kk] = ha[kk * L + row];
+    tl[kk] = tm[kk * L + row];
+    tx[kk] = ta[kk * L + row];
+  }
+#pragma unroll
+  for (int kk = 0; kk < C; ++kk) {
+    const int r0 = kk * L;
+    if (!FULL && r0 >= ntok) break;
+    const int r1 = FULL ? r0 + L : min(r0 + L, ntok);
+    const bool st = vr_bit(w, r0);
+    const bool nb = vr_popc_range(w, r0 + 1, r1) > 0;
+    if (!st) {  // the range's head continues the current piece (strict >: earlier tokens win)
+      if (!f.seen) {
+        if (h[kk] > f.thm) {
+          f.thm = h[kk];
+          f.tha = hx[kk];
+        }
+      } else if (h[kk] > f.pm) {
+        f.pm = h[kk];
+        f.pa = hx[kk];
+      }
+    }
+    if (st || nb) {  // the current piece ends at the range's first start
+      if (f.seen) vr_emit(p, rbase, f.pd, f.pm, f.pa - f.plast);
+      f.seen = true;
+      f.plast = vr_last_bit(w, r0, r1);
+      f.pd = d_first + vr_popc_range(w, 1, r1);
+      f.pm = tl[kk];
+      f.pa = tx[kk];
+    }
   }
 }
 
@@ -242,6 +304,7 @@ MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh
   constexpr int L = kVrTile / C;
   const int row = j * 32 + (int)lane;
   if (j * 32 >= p.n_cols) return;
+  const long long rbase = vr_row_base(p, row);
   float cm = -INFINITY;
   long long ca = 0, cd = -1, cs = 0;
   for (int t = 0; t < n_tiles; ++t) {
@@ -255,57 +318,30 @@ MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh
     const long long d_first = sh->info[islot].d_first;
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->iempty[islot]);
-    const int set = t & 1, pb = (t >> 1) & 1;
-    mbar_wait(&hdr->pfull[set][pb], ((uint32_t)t >> 2) & 1u);
-    bool seen = false;       // a document starts somewhere in [0, ntok)
-    float thm = -INFINITY;   // tile head: tokens before the first start (the carried document)
-    int tha = 0;
-    float pm = -INFINITY;    // piece after the latest start
-    int pa = 0, plast = 0;
-#pragma unroll
-    for (int kk = 0; kk < C; ++kk) {
-      const int r0 = kk * L;
-      if (r0 < ntok) {
-        const int r1 = min(r0 + L, ntok);
-        const bool st = vr_bit(w, r0);
-        const int nb = vr_popc_range(w, r0 + 1, r1);
-        if (!st) {  // the range's head continues the current piece
-          const float h = sh->hm[set][pb][kk][row];
-          const int hx = sh->ha[set][pb][kk][row];
-          if (!seen) {
-            if (h > thm) {
-              thm = h;
-              tha = hx;
-            }
-          } else if (h > pm) {
-            pm = h;
-            pa = hx;
-          }
-        }
-        if (st || nb > 0) {  // the current piece ends at the range's first start
-          if (seen) vr_emit(p, row, d_first + vr_popc_range(w, 1, plast + 1), pm, pa - plast);
-          seen = true;
-          plast = vr_last_bit(w, r0, r1);
-          pm = sh->tm[set][pb][kk][row];
-          pa = sh->ta[set][pb][kk][row];
-        }
-      }
-    }
+    const int set = t & 1, pb = (t >> 1) % kVrPieceBufs;
+    mbar_wait(&hdr->pfull[set][pb], (((uint32_t)t >> 1) / kVrPieceBufs) & 1u);
+    VrTileFold f;
+    if (ntok == kVrTile)
+      vr_fold_ranges<C, true>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
+                              kVrTile, row, p, rbase);
+    else
+      vr_fold_ranges<C, false>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
+                               ntok, row, p, rbase);
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->pempty[set][pb]);
-    if (!vr_bit(w, 0) && (thm > cm || cd < 0)) {  // the tile head continues the carried document
-      cm = thm;
-      ca = p0 + tha;
+    if (!vr_bit(w, 0) && (f.thm > cm || cd < 0)) {  // the tile head continues the carried document
+      cm = f.thm;
+      ca = p0 + f.tha;
     }
-    if (seen) {  // the carried document ended at the tile's first start
-      vr_emit(p, row, cd, cm, ca - cs);
-      cm = pm;
-      ca = p0 + pa;
-      cd = d_first + vr_popc_range(w, 1, plast + 1);
-      cs = p0 + plast;
+    if (f.seen) {  // the carried document ended at the tile's first start
+      vr_emit(p, rbase, cd, cm, ca - cs);
+      cm = f.pm;
+      ca = p0 + f.pa;
+      cd = f.pd;
+      cs = p0 + f.plast;
     }
   }
-  if (n_tiles > 0) vr_emit(p, row, cd, cm, ca - cs);  // the CTA's last document ends at tok_end
+  if (n_tiles > 0) vr_emit(p, rbase, cd, cm, ca - cs);  // the CTA's last document ends at tok_end
 }
 
 template <TcKind KIND, int KA>
@@ -351,7 +387,7 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       mbar_init(&hdr->iempty[s], (uint32_t)(n_active + n_merge));  // scan warps of the set + merge warps
     }
     for (int s = 0; s < 2; ++s)
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < kVrPieceBufs; ++b) {
         mbar_init(&hdr->pfull[s][b], (uint32_t)n_active);
         mbar_init(&hdr->pempty[s][b], (uint32_t)n_merge);
       }
