@@ -318,8 +318,36 @@ int launch_fwd_exact(const void* Q, int64_t n_q, int64_t l_q, const void* D, int
 
 // Vectorised gather dispatch: rows must be 8-byte aligned (dim * sizeof(T) % 8 == 0) and the
 // dimension must fit NP <= 4 passes of 32 lanes x 8 bytes; otherwise the scalar kernels run.
+// Row-group kernels when a row is exactly 8, 16 or 32 lanes x 16 B (bf16/f16 d = 64/128/256,
+// f32 d = 32/64/128).
+template <typename T>
+static int rowgroup_lanes(int dim) {
+  const int bytes = dim * (int)sizeof(T);
+  if (bytes % 16) return 0;
+  const int lpr = bytes / 16;
+  return (lpr == 8 || lpr == 16 || lpr == 32) ? lpr : 0;
+}
+template <typename T>
+static bool launch_grad_docs_rg(const T* Q, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  switch (rowgroup_lanes<T>(p.dim)) {
+    case 8: mxs::grad_docs_rg_kernel<T, 8><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    case 16: mxs::grad_docs_rg_kernel<T, 16><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    case 32: mxs::grad_docs_rg_kernel<T, 32><<<(unsigned)blocks, 256, 0, st>>>(Q, p); return true;
+    default: return false;
+  }
+}
+template <typename T>
+static bool launch_grad_query_rg(const T* D, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  switch (rowgroup_lanes<T>(p.dim)) {
+    case 8: mxs::grad_query_rg_kernel<T, 8><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    case 16: mxs::grad_query_rg_kernel<T, 16><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    case 32: mxs::grad_query_rg_kernel<T, 32><<<(unsigned)blocks, 256, 0, st>>>(D, p); return true;
+    default: return false;
+  }
+}
 template <typename T>
 static bool launch_grad_docs_vec(const T* Q, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  if (launch_grad_docs_rg<T>(Q, p, blocks, st)) return true;
   constexpr int V = mxs::Vec8<T>::N;
   if ((p.dim * (int)sizeof(T)) % 8 != 0) return false;
   const int np = (p.dim + 32 * V - 1) / (32 * V);
@@ -333,6 +361,7 @@ static bool launch_grad_docs_vec(const T* Q, const mxs::GradParams& p, long long
 }
 template <typename T>
 static bool launch_grad_query_vec(const T* D, const mxs::GradParams& p, long long blocks, cudaStream_t st) {
+  if (launch_grad_query_rg<T>(D, p, blocks, st)) return true;
   constexpr int V = mxs::Vec8<T>::N;
   if ((p.dim * (int)sizeof(T)) % 8 != 0) return false;
   const int np = (p.dim + 32 * V - 1) / (32 * V);

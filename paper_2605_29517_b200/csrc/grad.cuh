@@ -163,17 +163,18 @@ __global__ void __launch_bounds__(256) grad_docs_vec_kernel(const T* __restrict_
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[a][v] = 0.f;
   const int lo = __ldg(p.row_ptr + r), hi = __ldg(p.row_ptr + r + 1);
-  const long long per_q = (long long)p.n_docs * p.l_q;
+  // source ids are < 2^31 (checked on the host): 32-bit unsigned decode
+  const uint32_t per_q = (uint32_t)p.n_docs * (uint32_t)p.l_q, lq = (uint32_t)p.l_q;
   for (int t0 = lo; t0 < hi; t0 += 32) {
     const int n = min(32, hi - t0);
     // lane j decodes source t0 + j: Q row and weight
     long long my_row = 0;
     float my_w = 0.f;
     if (lane < n) {
-      const long long s = __ldg(p.col_idx + t0 + lane);
-      const int q = (int)(s / per_q);
-      const int b = (int)((s / p.l_q) % p.n_docs);
-      my_row = (long long)q * p.l_q + s % p.l_q;
+      const uint32_t s = (uint32_t)__ldg(p.col_idx + t0 + lane);
+      const uint32_t q = s / per_q, rem = s - q * per_q;
+      const uint32_t b = rem / lq, i = rem - b * lq;
+      my_row = (long long)q * lq + i;
       my_w = __ldg(p.g + (long long)q * p.n_docs + b);
     }
     for (int j0 = 0; j0 < n; j0 += kGradU) {
@@ -276,6 +277,158 @@ __global__ void __launch_bounds__(256) grad_query_vec_kernel(const T* __restrict
         *reinterpret_cast<float2*>(out + k) = make_float2(acc[a][0], acc[a][1]);
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Row-group variants: a gathered row is covered by LPR lanes x 16 B, so one warp load instruction
+// moves SP = 32 / LPR source rows (d = 128 bf16: two 256-B rows per LDG.128).  Lane group h
+// accumulates the sources j = h (mod SP) in order (fp32, FFMA2); the SP partial sums are added
+// in a fixed order at the end -- deterministic, no atomics, still destination-owned.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  MXS_DEV static void load(const __nv_bfloat16* p, float (&o)[8]) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      o[2 * i] = __uint_as_float(w[i] << 16);
+      o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct Vec16<__half> {
+  static constexpr int N = 8;
+  MXS_DEV static void load(const __half* p, float (&o)[8]) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+  }
+};
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+  MXS_DEV static void load(const float* p, float (&o)[4]) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+    o[2] = t.z;
+    o[3] = t.w;
+  }
+};
+
+constexpr int kGradGU = 4;  // source rows in flight per lane group
+
+template <typename T, int LPR>
+MXS_DEV void grad_rowgroup_accum(const T* __restrict__ base, int dim, const long long (&rows)[kGradGU],
+                                 const float (&ws)[kGradGU], float (&acc)[Vec16<T>::N], int lp) {
+  constexpr int V = Vec16<T>::N;
+  float x[kGradGU][V];
+#pragma unroll
+  for (int u = 0; u < kGradGU; ++u) Vec16<T>::load(base + rows[u] * dim + lp * V, x[u]);
+#pragma unroll
+  for (int u = 0; u < kGradGU; ++u)
+#pragma unroll
+    for (int v = 0; v < V; v += 2) ffma2_rn(acc[v], acc[v + 1], ws[u], ws[u], x[u][v], x[u][v + 1]);
+}
+
+template <typename T, int LPR>
+MXS_DEV void grad_rowgroup_store(float (&acc)[Vec16<T>::N], float* out, int lane) {
+  constexpr int V = Vec16<T>::N;
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+  if (lane < LPR) {
+#pragma unroll
+    for (int v = 0; v < V; v += 4)
+      *reinterpret_cast<float4*>(out + lane * V + v) = make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]);
+  }
+}
+
+// K7 row-group: warp per destination row (CSR bucket), dim = LPR * V.
+template <typename T, int LPR>
+__global__ void __launch_bounds__(256) grad_docs_rg_kernel(const T* __restrict__ Q, const GradParams p) {
+  constexpr int V = Vec16<T>::N, SP = 32 / LPR;
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, h = lane / LPR, lp = lane % LPR;
+  if (r >= p.n_dest) return;
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  const int lo = __ldg(p.row_ptr + r), hi = __ldg(p.row_ptr + r + 1);
+  const uint32_t per_q = (uint32_t)p.n_docs * (uint32_t)p.l_q, lq = (uint32_t)p.l_q;
+  for (int t0 = lo; t0 < hi; t0 += 32) {
+    const int n = min(32, hi - t0);
+    int my_row = 0;
+    float my_w = 0.f;
+    if (lane < n) {
+      const uint32_t s = (uint32_t)__ldg(p.col_idx + t0 + lane);
+      const uint32_t q = s / per_q, rem = s - q * per_q;
+      const uint32_t b = rem / lq, i = rem - b * lq;
+      my_row = (int)(q * lq + i);
+      my_w = __ldg(p.g + (long long)q * p.n_docs + b);
+    }
+    for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
+      long long rows[kGradGU];
+      float ws[kGradGU];
+#pragma unroll
+      for (int u = 0; u < kGradGU; ++u) {
+        const int j = j0 + u * SP + h;
+        const int rr = __shfl_sync(0xffffffffu, my_row, j & 31);
+        const float ww = __shfl_sync(0xffffffffu, my_w, j & 31);
+        rows[u] = (j < n) ? rr : 0;
+        ws[u] = (j < n) ? ww : 0.f;
+      }
+      grad_rowgroup_accum<T, LPR>(Q, p.dim, rows, ws, acc, lp);
+    }
+  }
+  grad_rowgroup_store<T, LPR>(acc, p.dD + r * p.dim, lane);
+}
+
+// K8 row-group: warp per (q, i) query row, documents b ascending.
+template <typename T, int LPR>
+__global__ void __launch_bounds__(256) grad_query_rg_kernel(const T* __restrict__ D, const GradParams p) {
+  constexpr int V = Vec16<T>::N, SP = 32 / LPR;
+  const long long wq = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, h = lane / LPR, lp = lane % LPR;
+  if (wq >= (long long)p.n_q * p.l_q) return;
+  const int q = (int)(wq / p.l_q), i = (int)(wq % p.l_q);
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  for (int b0 = 0; b0 < p.n_docs; b0 += 32) {
+    const int n = min(32, p.n_docs - b0);
+    long long my_row = 0;
+    float my_w = 0.f;
+    if (lane < n) {
+      const int a_ = __ldg(p.argmax + ((long long)q * p.n_docs + b0 + lane) * p.l_q + i);
+      my_w = __ldg(p.g + (long long)q * p.n_docs + b0 + lane);
+      my_row = __ldg(p.doc_row_off + b0 + lane) + a_;
+    }
+    for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
+      long long rows[kGradGU];
+      float ws[kGradGU];
+#pragma unroll
+      for (int u = 0; u < kGradGU; ++u) {
+        const int j = j0 + u * SP + h;
+        const long long rr = __shfl_sync(0xffffffffu, my_row, j & 31);
+        const float ww = __shfl_sync(0xffffffffu, my_w, j & 31);
+        rows[u] = (j < n) ? rr : 0;
+        ws[u] = (j < n) ? ww : 0.f;
+      }
+      grad_rowgroup_accum<T, LPR>(D, p.dim, rows, ws, acc, lp);
+    }
+  }
+  grad_rowgroup_store<T, LPR>(acc, p.dQ + wq * p.dim, lane);
 }
 
 }  // namespace mxs

@@ -254,6 +254,15 @@ MXS_DEV void fadd2_rn(float& o0, float& o1, float a0, float a1, float b0, float 
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(o0), "=f"(o1) : "l"(d));
 }
+// Packed fp32 pair FMA (FFMA2), round-to-nearest, single rounding per lane: {a*b+c}.
+MXS_DEV void ffma2_rn(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  unsigned long long a, b, c, d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(d0), "f"(d1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
 // Exact int32 -> fp32 for |x| <= 2^22 without the XU conversion pipe: x + 0x4B400000 is the
 // bit pattern of 1.5 * 2^23 + x (same binade, or 2^24 exactly at x = 2^22), so one integer add
 // on the ALU pipe plus one FADD (packed, below) recovers x exactly.
