@@ -529,6 +529,7 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
   std::call_once(once, [] {
     cudaFuncSetAttribute(mxs::csr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(mxs::csr_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mxs::csr_place_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const unsigned segs = (unsigned)(n_q * n_docs);
   // rows that belong to no document (never the case for padded / packed layouts) stay zero
@@ -541,7 +542,10 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
   if ((s = check_launch("csr_count_kernel")) != MXS_OK) return s;
   mxs::csr_scan_kernel<<<(unsigned)n_docs, 1024, 0, st>>>(p);
   if ((s = check_launch("csr_scan_kernel")) != MXS_OK) return s;
-  mxs::csr_place_kernel<<<segs, 256, hist_bytes, st>>>(p);
+  if (hist_bytes * mxs::kCsrWarps <= 200 * 1024)
+    mxs::csr_place_v2_kernel<<<segs, 32 * mxs::kCsrWarps, hist_bytes * mxs::kCsrWarps, st>>>(p);
+  else
+    mxs::csr_place_kernel<<<segs, 256, hist_bytes, st>>>(p);
   return check_launch("csr_place_kernel");
 }
 

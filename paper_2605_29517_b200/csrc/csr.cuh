@@ -128,4 +128,54 @@ __global__ void __launch_bounds__(256) csr_place_kernel(const CsrParams p) {
   }
 }
 
+// Placement v2: one block per (q, b) segment, 8 warps on contiguous source chunks.  Per-warp
+// bucket histograms in shared memory turn the cross-warp order into prefix offsets, so every
+// warp places its chunk independently (in-warp order from __match_any_sync ranks) -- two block
+// barriers per segment instead of one per warp turn.
+constexpr int kCsrWarps = 8;
+__global__ void __launch_bounds__(32 * kCsrWarps) csr_place_v2_kernel(const CsrParams p) {
+  extern __shared__ int32_t hw[];  // [kCsrWarps][len]
+  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < kCsrWarps * len; t += blockDim.x) hw[t] = 0;
+  __syncthreads();
+  const long long src0 = ((long long)q * p.n_docs + b) * p.l_q;
+  const int32_t* a = p.argmax + src0;
+  const int chunk = ((p.l_q + kCsrWarps - 1) / kCsrWarps + 31) & ~31;
+  const int e0 = w * chunk, e1 = min(p.l_q, e0 + chunk);
+  int32_t* h = hw + w * len;
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const int key = __ldg(a + e);
+    if (key >= 0 && key < len) atomicAdd(&h[key], 1);
+  }
+  __syncthreads();
+  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;  // first slot of (q, b) per bucket
+  for (int r = threadIdx.x; r < len; r += blockDim.x) {
+    int run = base[r];
+#pragma unroll
+    for (int ww = 0; ww < kCsrWarps; ++ww) {
+      const int v = hw[ww * len + r];
+      hw[ww * len + r] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int e = e0; e < e1; e += 32) {
+    const int i = e + lane;
+    const bool valid = i < e1;
+    int key = valid ? __ldg(a + i) : -1;
+    const bool ok = valid && key >= 0 && key < len;
+    if (!ok) key = -1 - lane;  // distinct dummy keys never match real ones
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int rank = __popc(peers & lt_mask);
+    if (ok) p.col_idx[h[key] + rank] = (int32_t)(src0 + i);
+    __syncwarp();
+    if (ok && rank == 0) h[key] += __popc(peers);
+    __syncwarp();
+  }
+}
+
 }  // namespace mxs
