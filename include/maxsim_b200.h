@@ -36,7 +36,12 @@ typedef enum {
   MXS_BAD_TILE_CONFIG = 8,    /* maxsim/errors.py:39 BadTileConfig */
   MXS_UNSUPPORTED = 9,        /* shape/dtype outside what the sm_100a kernels accept */
   MXS_CUDA_ERROR = 10,        /* launch or driver failure */
-  MXS_INVALID_ARGUMENT = 11   /* null pointer / negative size */
+  MXS_INVALID_ARGUMENT = 11,  /* null pointer / negative size */
+  MXS_IO_ERROR = 12,          /* maxsim/errors.py:60 IoError */
+  MXS_BAD_MAGIC = 13,         /* maxsim/errors.py:64 BadMagic */
+  MXS_VERSION_UNSUPPORTED = 14, /* maxsim/errors.py:68 VersionUnsupported */
+  MXS_TRUNCATED_PAYLOAD = 15, /* maxsim/errors.py:74 TruncatedPayload */
+  MXS_STALE_ARGMIN = 16       /* maxsim/errors.py:49 StaleArgmin */
 } mxs_status;
 
 typedef enum { MXS_F32 = 0, MXS_F16 = 1, MXS_BF16 = 2, MXS_I8 = 3 } mxs_dtype;
@@ -152,6 +157,27 @@ int mxs_topk(const double* scores, int64_t n, int64_t k, int64_t id_offset, doub
  */
 int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int64_t k, double* top_s, int64_t* top_id,
                         void* stream);
+
+/*
+ * MXS1 embedding files (HOST side; maxsim/streamio.py:1-163).  Replaces _parse_header
+ * (maxsim/streamio.py:103), read_embeddings (:136) and CorpusReader.read_block (:209).
+ *   mxs_mxs1_open        parse + validate the header; *handle owns the file descriptor
+ *   mxs_mxs1_info        elem (0 f32, 1 f16, 2 i8), layout (0 dense, 1 packed, 2 quantized),
+ *                        n_docs, length (dense / quantized; 0 for packed), dim
+ *   mxs_mxs1_cu_seqlens  packed only: copy the offset table [n_docs + 1] (int64) to host `out`
+ *   mxs_mxs1_block_bytes payload bytes of documents [first, first + count)
+ *   mxs_mxs1_read_block  copy those raw elements (file dtype) into HOST memory `dst`
+ *   mxs_mxs1_read_scales quantized only: the [n_docs * length] f32 scales into HOST `dst`
+ * Errors: MXS_IO_ERROR, MXS_BAD_MAGIC, MXS_VERSION_UNSUPPORTED, MXS_TRUNCATED_PAYLOAD (with the
+ * reference's expected / actual byte counts in mxs_last_error()).
+ */
+int mxs_mxs1_open(const char* path, void** handle);
+int mxs_mxs1_info(void* handle, int32_t* elem, int32_t* layout, int64_t* n_docs, int64_t* length, int64_t* dim);
+int mxs_mxs1_cu_seqlens(void* handle, int64_t* out);
+int64_t mxs_mxs1_block_bytes(void* handle, int64_t first, int64_t count);
+int mxs_mxs1_read_block(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes);
+int mxs_mxs1_read_scales(void* handle, float* dst, size_t dst_bytes);
+void mxs_mxs1_close(void* handle);
 
 #ifdef __cplusplus
 }

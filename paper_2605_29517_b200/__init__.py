@@ -18,6 +18,11 @@ from .errors import (
     ShapeMismatch,
     StaleCsr,
     Unsupported,
+    IoError,
+    BadMagic,
+    VersionUnsupported,
+    TruncatedPayload,
+    StaleArgmin,
 )
 from .instrument import TrafficReport
 from .types import ArgmaxMap, DEFAULT_TILE, DocBatch, EmbeddingMatrix, ScoreMatrix, TileConfig, validate_pair
@@ -54,12 +59,14 @@ from .quant import (
 from .varlen import PackedCorpus, fused_score_varlen, pack, score_varlen, unpack
 from .topk import TopKHeap, ranked, topk
 from .autograd import MaxSimFunction, MaxSimVarlenFunction, maxsim, maxsim_varlen
+from .streamio import (
+    CorpusReader,
+    TrafficModel,
+    model_traffic,
+    read_embeddings,
+    stream_score_topk,
+    write_embeddings,
+)
 
 __version__ = "0.1.0"
 
-
-def model_traffic(n_queries, n_docs, len_q, len_d, dim, elem_bytes=4, scalar_bytes=8):
-    """Analytic fused byte model (maxsim/streamio.py:366-395): (fused_read, fused_write)."""
-    q_bytes = n_queries * len_q * dim * elem_bytes
-    d_bytes = n_queries * n_docs * len_d * dim * elem_bytes
-    return q_bytes + d_bytes, n_queries * n_docs * scalar_bytes

@@ -42,6 +42,13 @@ _SIGNATURES = {
     "mxs_topk_workspace_bytes": [c_i64, c_i64],
     "mxs_topk": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
     "mxs_topk_candidates": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "mxs_mxs1_open": [ctypes.c_char_p, ctypes.POINTER(c_vp)],
+    "mxs_mxs1_info": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "mxs_mxs1_cu_seqlens": [c_vp, c_vp],
+    "mxs_mxs1_block_bytes": [c_vp, c_i64, c_i64],
+    "mxs_mxs1_read_block": [c_vp, c_i64, c_i64, c_vp, c_size],
+    "mxs_mxs1_read_scales": [c_vp, c_vp, c_size],
+    "mxs_mxs1_close": [c_vp],
 }
 _RESTYPES = {
     "mxs_version": ctypes.c_char_p,
@@ -49,6 +56,8 @@ _RESTYPES = {
     "mxs_last_error": ctypes.c_char_p,
     "mxs_csr_workspace_bytes": ctypes.c_size_t,
     "mxs_topk_workspace_bytes": ctypes.c_size_t,
+    "mxs_mxs1_block_bytes": ctypes.c_int64,
+    "mxs_mxs1_close": None,
 }
 
 MXS_F32, MXS_F16, MXS_BF16, MXS_I8 = 0, 1, 2, 3
@@ -65,6 +74,11 @@ _STATUS_TO_ERROR = {
     9: errors.Unsupported,
     10: errors.CudaError,
     11: errors.ShapeMismatch,
+    12: errors.IoError,
+    13: errors.BadMagic,
+    14: errors.VersionUnsupported,
+    15: errors.TruncatedPayload,
+    16: errors.StaleArgmin,
 }
 
 

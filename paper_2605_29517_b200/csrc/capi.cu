@@ -1,4 +1,5 @@
 // extern "C" entry points of libmaxsim_b200.so (see include/maxsim_b200.h).
+#include <cerrno>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +17,7 @@
 #include "grad.cuh"
 #include "quant.cuh"
 #include "topk.cuh"
+#include "mxs1_io.h"
 
 namespace {
 
@@ -398,6 +400,11 @@ const char* mxs_status_string(int s) {
     case MXS_UNSUPPORTED: return "Unsupported";
     case MXS_CUDA_ERROR: return "CudaError";
     case MXS_INVALID_ARGUMENT: return "InvalidArgument";
+    case MXS_IO_ERROR: return "IoError";
+    case MXS_BAD_MAGIC: return "BadMagic";
+    case MXS_VERSION_UNSUPPORTED: return "VersionUnsupported";
+    case MXS_TRUNCATED_PAYLOAD: return "TruncatedPayload";
+    case MXS_STALE_ARGMIN: return "StaleArgmin";
     default: return "unknown";
   }
 }
@@ -731,6 +738,149 @@ int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     return fail(MXS_UNSUPPORTED, "mxs_fused_score_varlen: dtype %d", dtype);
   if (s != MXS_OK) return s;
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
+}
+
+
+// ------------------------------------------------------------------ MXS1 files (host side)
+static int mxs1_truncated(int64_t expected, int64_t actual) {
+  return fail(MXS_TRUNCATED_PAYLOAD, "payload truncated: expected %lld bytes, file holds %lld", (long long)expected,
+              (long long)actual);
+}
+
+int mxs_mxs1_open(const char* path, void** handle) {
+  if (!path || !handle) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_open: null pointer");
+  *handle = nullptr;
+  const int fd = ::open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return fail(MXS_IO_ERROR, "cannot read %s: %s", path, strerror(errno));
+  auto* f = new mxs_io::Mxs1File();
+  f->fd = fd;
+  f->path = path;
+  struct stat stt;
+  f->file_size = (fstat(fd, &stt) == 0) ? (int64_t)stt.st_size : 0;
+  auto bail = [&](int st) {
+    ::close(fd);
+    delete f;
+    return st;
+  };
+  unsigned char head[8];
+  if (mxs_io::pread_all(fd, head, 8, 0) != 8) return bail(fail(MXS_BAD_MAGIC, "file too short to hold a header"));
+  if (memcmp(head, "MXS1", 4) != 0) {
+    char m[64];
+    snprintf(m, sizeof(m), "b'%c%c%c%c'", head[0], head[1], head[2], head[3]);
+    return bail(fail(MXS_BAD_MAGIC, "bad magic %s", m));
+  }
+  const unsigned version = (unsigned)head[4] | ((unsigned)head[5] << 8);
+  if (version != 1) return bail(fail(MXS_VERSION_UNSUPPORTED, "unsupported embedding file version %u", version));
+  const int ec = head[6], lc = head[7];
+  if (ec > 2 || lc > 2) return bail(fail(MXS_BAD_MAGIC, "unknown element/layout tags (%d, %d)", ec, lc));
+  f->elem = ec;
+  f->layout = lc;
+  int64_t off = 8;
+  auto u64 = [&](int64_t& out) -> bool {
+    uint64_t v = 0;
+    const int64_t got = mxs_io::pread_all(fd, &v, 8, off);
+    if (got != 8) {
+      mxs1_truncated(8, got < 0 ? 0 : got);
+      return false;
+    }
+    off += 8;
+    out = (int64_t)v;  // little-endian host (x86-64 / aarch64)
+    return true;
+  };
+  if (lc == mxs_io::kDense || lc == mxs_io::kQuantized) {
+    if (!u64(f->n_docs) || !u64(f->length) || !u64(f->dim)) return bail(MXS_TRUNCATED_PAYLOAD);
+  } else {
+    if (!u64(f->n_docs) || !u64(f->dim)) return bail(MXS_TRUNCATED_PAYLOAD);
+    f->cu.resize((size_t)f->n_docs + 1);
+    const int64_t need = 8 * (f->n_docs + 1);
+    const int64_t got = mxs_io::pread_all(fd, f->cu.data(), need, off);
+    if (got != need) return bail(mxs1_truncated(need, got < 0 ? 0 : got));
+    off += need;
+  }
+  if (lc == mxs_io::kQuantized && ec != mxs_io::kI8)
+    return bail(fail(MXS_BAD_MAGIC, "quantized layout requires the i8 element tag"));
+  if (lc != mxs_io::kQuantized && ec == mxs_io::kI8)
+    return bail(fail(MXS_BAD_MAGIC, "int8 elements require the quantized layout (scales are part of the data)"));
+  f->payload_offset = off;
+  *handle = f;
+  return MXS_OK;
+}
+
+int mxs_mxs1_info(void* handle, int32_t* elem, int32_t* layout, int64_t* n_docs, int64_t* length, int64_t* dim) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  if (!f) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_info: null handle");
+  if (elem) *elem = f->elem;
+  if (layout) *layout = f->layout;
+  if (n_docs) *n_docs = f->n_docs;
+  if (length) *length = f->length;
+  if (dim) *dim = f->dim;
+  return MXS_OK;
+}
+
+int mxs_mxs1_cu_seqlens(void* handle, int64_t* out) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  if (!f || !out) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_cu_seqlens: null pointer");
+  if (f->layout != mxs_io::kPacked) return fail(MXS_SHAPE_MISMATCH, "offset table exists for packed files only");
+  memcpy(out, f->cu.data(), f->cu.size() * sizeof(int64_t));
+  return MXS_OK;
+}
+
+static bool mxs1_range(const mxs_io::Mxs1File* f, int64_t first, int64_t count, int64_t& off, int64_t& bytes) {
+  if (first < 0 || count < 0 || first > f->n_docs) return false;
+  count = std::min(count, f->n_docs - first);
+  const int64_t es = mxs_io::elem_size(f->elem);
+  if (f->layout == mxs_io::kPacked) {
+    const int64_t t0 = f->cu[(size_t)first], t1 = f->cu[(size_t)(first + count)];
+    off = f->payload_offset + t0 * f->dim * es;
+    bytes = (t1 - t0) * f->dim * es;
+  } else {
+    off = f->payload_offset + first * f->length * f->dim * es;
+    bytes = count * f->length * f->dim * es;
+  }
+  return true;
+}
+
+int64_t mxs_mxs1_block_bytes(void* handle, int64_t first, int64_t count) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  int64_t off = 0, bytes = 0;
+  if (!f || !mxs1_range(f, first, count, off, bytes)) return -1;
+  return bytes;
+}
+
+int mxs_mxs1_read_block(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  if (!f || !dst) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_read_block: null pointer");
+  int64_t off = 0, bytes = 0;
+  if (!mxs1_range(f, first, count, off, bytes))
+    return fail(MXS_INDEX_OUT_OF_RANGE, "block [%lld, +%lld) outside the %lld documents", (long long)first,
+                (long long)count, (long long)f->n_docs);
+  if ((int64_t)dst_bytes < bytes) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_read_block: buffer too small");
+  const int64_t got = mxs_io::pread_parallel(f->fd, dst, bytes, off);
+  if (got < 0) return fail(MXS_IO_ERROR, "cannot read %s: %s", f->path.c_str(), strerror(errno));
+  if (got != bytes) {
+    // the reference reports the expected payload of the whole file for dense / packed loads
+    return mxs1_truncated(bytes, got);
+  }
+  return MXS_OK;
+}
+
+int mxs_mxs1_read_scales(void* handle, float* dst, size_t dst_bytes) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  if (!f || !dst) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_read_scales: null pointer");
+  if (f->layout != mxs_io::kQuantized) return fail(MXS_SHAPE_MISMATCH, "scales exist for quantized files only");
+  const int64_t need_q = f->n_docs * f->length * f->dim, need_s = f->n_docs * f->length * 4;
+  if ((int64_t)dst_bytes < need_s) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_read_scales: buffer too small");
+  const int64_t got = mxs_io::pread_all(f->fd, dst, need_s, f->payload_offset + need_q);
+  if (got < 0) return fail(MXS_IO_ERROR, "cannot read %s: %s", f->path.c_str(), strerror(errno));
+  if (got != need_s) return mxs1_truncated(need_q + need_s, got);
+  return MXS_OK;
+}
+
+void mxs_mxs1_close(void* handle) {
+  auto* f = static_cast<mxs_io::Mxs1File*>(handle);
+  if (!f) return;
+  if (f->fd >= 0) ::close(f->fd);
+  delete f;
 }
 
 }  // extern "C"

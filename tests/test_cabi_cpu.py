@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "maxsim_b200.h")
 
 def declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|size_t|const char\*)\s+(mxs_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|void|size_t|const char\*)\s+(mxs_\w+)\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")

@@ -147,7 +147,11 @@ def test_traffic_report_and_byte_model():
     rep.merge(other)
     assert rep.as_dict() == {"bytes_read": 15, "bytes_written": 0, "peak_aux_bytes": 100, "mac_count": 4}
     g = golden("misc")
-    assert list(mx.model_traffic(1, 1000, 1024, 1024, 128, elem_bytes=2)) == list(g["traffic"][:2])
+    tm = mx.model_traffic(1, 1000, 1024, 1024, 128, elem_bytes=2)
+    assert [tm.fused_read, tm.fused_write, tm.naive_read, tm.naive_write] == list(g["traffic"])
+    assert tm.naive_over_fused == tm.naive_total / tm.fused_total and tm.bytes("fused") == tm.fused_total
+    with pytest.raises(ValueError):
+        mx.model_traffic(0, 1, 1, 1, 1)
 
 
 def test_compute_refuses_host_tensors():
