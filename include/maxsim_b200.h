@@ -159,6 +159,21 @@ int mxs_topk_candidates(const double* scores, const int64_t* ids, int64_t n, int
                         void* stream);
 
 /*
+ * Chamfer distance (maxsim/chamfer.py:49-199), float32 bit-exact with the reference.
+ *   mxs_sq_norms       X [rows, dim] f32 -> out [rows] f32 (maxsim/kernels.py:41 sq_norms)
+ *   mxs_chamfer_nn     per point of A: min over B of |a|^2 + |b|^2 - 2<a,b> (reference order)
+ *                      and the lowest argmin (maxsim/chamfer.py:49 _nearest_fold); dim <= 16
+ *   mxs_chamfer_grad   one side of chamfer_backward (maxsim/chamfer.py:167): float64
+ *                      dX[r] = c_gather (x_r - y_nn[r]) + sum over CSR bucket r of c_scatter (x_r - y_j)
+ */
+int mxs_sq_norms(const float* X, int64_t rows, int64_t dim, float* out, void* stream);
+int mxs_chamfer_nn(const float* A, const float* a_norms, int64_t n, const float* B, const float* b_norms, int64_t m,
+                   int64_t dim, float* best, int32_t* idx, void* stream);
+int mxs_chamfer_grad(const float* X, int64_t nx, const float* Y, int64_t dim, const int32_t* nn,
+                     const int32_t* row_ptr, const int32_t* col_idx, double c_gather, double c_scatter, double* dX,
+                     void* stream);
+
+/*
  * MXS1 embedding files (HOST side; maxsim/streamio.py:1-163).  Replaces _parse_header
  * (maxsim/streamio.py:103), read_embeddings (:136) and CorpusReader.read_block (:209).
  *   mxs_mxs1_open        parse + validate the header; *handle owns the file descriptor

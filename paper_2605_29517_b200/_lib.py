@@ -42,6 +42,9 @@ _SIGNATURES = {
     "mxs_topk_workspace_bytes": [c_i64, c_i64],
     "mxs_topk": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
     "mxs_topk_candidates": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "mxs_sq_norms": [c_vp, c_i64, c_i64, c_vp, c_vp],
+    "mxs_chamfer_nn": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "mxs_chamfer_grad": [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_vp, c_vp],
     "mxs_mxs1_open": [ctypes.c_char_p, ctypes.POINTER(c_vp)],
     "mxs_mxs1_info": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "mxs_mxs1_cu_seqlens": [c_vp, c_vp],

@@ -18,6 +18,7 @@
 #include "quant.cuh"
 #include "topk.cuh"
 #include "mxs1_io.h"
+#include "chamfer.cuh"
 
 namespace {
 
@@ -740,6 +741,42 @@ int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
 }
 
+
+// ------------------------------------------------------------------ Chamfer
+int mxs_sq_norms(const float* X, int64_t rows, int64_t dim, float* out, void* stream) {
+  if (!X || !out) return fail(MXS_INVALID_ARGUMENT, "mxs_sq_norms: null pointer");
+  if (rows < 1 || dim < 1) return fail(MXS_SHAPE_MISMATCH, "mxs_sq_norms: empty input");
+  const long long blocks = (rows + 255) / 256;
+  mxs::sq_norms_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, rows, (int)dim, out);
+  return check_launch("sq_norms_kernel");
+}
+
+int mxs_chamfer_nn(const float* A, const float* a_norms, int64_t n, const float* B, const float* b_norms, int64_t m,
+                   int64_t dim, float* best, int32_t* idx, void* stream) {
+  if (!A || !a_norms || !B || !b_norms || !best || !idx) return fail(MXS_INVALID_ARGUMENT, "mxs_chamfer_nn: null");
+  if (n < 1 || m < 1) return fail(MXS_SHAPE_MISMATCH, "point set must hold at least one point");
+  if (dim < 1 || dim > mxs::kChDimMax) return fail(MXS_UNSUPPORTED, "mxs_chamfer_nn: dim %lld outside [1, 16]", (long long)dim);
+  if (m >= (1LL << 31)) return fail(MXS_UNSUPPORTED, "mxs_chamfer_nn: more than 2^31 points");
+  const long long blocks = (n + mxs::kChThreads - 1) / mxs::kChThreads;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dim == 3)
+    mxs::chamfer_nn_kernel<3><<<(unsigned)blocks, mxs::kChThreads, 0, st>>>(A, a_norms, n, B, b_norms, m, 3, best, idx);
+  else
+    mxs::chamfer_nn_kernel<0><<<(unsigned)blocks, mxs::kChThreads, 0, st>>>(A, a_norms, n, B, b_norms, m, (int)dim,
+                                                                            best, idx);
+  return check_launch("chamfer_nn_kernel");
+}
+
+int mxs_chamfer_grad(const float* X, int64_t nx, const float* Y, int64_t dim, const int32_t* nn,
+                     const int32_t* row_ptr, const int32_t* col_idx, double c_gather, double c_scatter, double* dX,
+                     void* stream) {
+  if (!X || !Y || !nn || !row_ptr || !col_idx || !dX) return fail(MXS_INVALID_ARGUMENT, "mxs_chamfer_grad: null");
+  if (nx < 1 || dim < 1) return fail(MXS_SHAPE_MISMATCH, "mxs_chamfer_grad: empty input");
+  const long long total = nx * dim, blocks = (total + 255) / 256;
+  mxs::chamfer_grad_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, nx, Y, (int)dim, nn, row_ptr,
+                                                                               col_idx, c_gather, c_scatter, dX);
+  return check_launch("chamfer_grad_kernel");
+}
 
 // ------------------------------------------------------------------ MXS1 files (host side)
 static int mxs1_truncated(int64_t expected, int64_t actual) {

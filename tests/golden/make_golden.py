@@ -216,12 +216,37 @@ def misc_cases():
          traffic=np.array([tm.fused_read, tm.fused_write, tm.naive_read, tm.naive_write], np.int64))
 
 
+def chamfer_cases():
+    """maxsim/chamfer.py: hand case (tests/test_chamfer.py:36-42), random clouds vs the dense
+    oracle (:51-63), ties (identical sets, :44-49), 5-D points, backward with upstream 1.7
+    (:109-118) -- forward and backward outputs of the reference itself."""
+    from maxsim import PointSet, chamfer_backward, chamfer_forward
+    from maxsim.synth import point_cloud
+
+    hp = PointSet([[0.0, 0.0, 0.0]])
+    hs = PointSet([[1.0, 0.0, 0.0], [0.0, 2.0, 0.0]])
+    hcd, ha1, ha2 = chamfer_forward(hp, hs)
+    p, s = point_cloud(200, seed=23), point_cloud(300, seed=24)
+    cd, a1, a2 = chamfer_forward(p, s)
+    dp, ds = chamfer_backward(p, s, a1, a2, upstream=1.7)
+    p5, s5 = point_cloud(70, seed=3, dim=5), point_cloud(45, seed=4, dim=5, scale=2.0)
+    cd5, b1, b2 = chamfer_forward(p5, s5)
+    dp5, ds5 = chamfer_backward(p5, s5, b1, b2)
+    # exact ties: duplicated points in the second set (lowest index must win)
+    rng = np.random.default_rng(8)
+    base = np.round(rng.standard_normal((20, 3)), 1).astype(np.float32)
+    tp = PointSet(base)
+    ts = PointSet(np.concatenate([base[::-1], base]).astype(np.float32))
+    cdt, t1, t2 = chamfer_forward(tp, ts)
+    save("chamfer", h_p=hp.data, h_s=hs.data, h_cd=np.float64(hcd), h_a1=ha1, h_a2=ha2, p=p.data, s=s.data,
+         cd=np.float64(cd), a1=a1, a2=a2, dp=dp, ds=ds, p5=p5.data, s5=s5.data, cd5=np.float64(cd5), b1=b1, b2=b2,
+         dp5=dp5, ds5=ds5, tp=tp.data, ts=ts.data, cdt=np.float64(cdt), t1=t1, t2=t2)
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
-    forward_cases()
-    synth_cases()
-    backward_cases()
-    quant_cases()
-    varlen_cases()
-    misc_cases()
+    cases = {"forward": forward_cases, "synth": synth_cases, "backward": backward_cases, "quant": quant_cases,
+             "varlen": varlen_cases, "misc": misc_cases, "chamfer": chamfer_cases}
+    for name in (sys.argv[1:] or list(cases)):
+        cases[name]()
     print("reference version", maxsim.__version__)

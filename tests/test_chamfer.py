@@ -1,0 +1,88 @@
+"""Chamfer distance (maxsim/chamfer.py) on the device against the REAL reference's outputs
+(tests/golden/chamfer.npz, tests/golden/make_golden.py chamfer): forward distance and argmins
+bit-identical (float32 arithmetic in the reference order, lowest index on ties), backward
+bit-identical (float64, reference accumulation order through the shared inverse CSR)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_29517_b200 as mx
+from conftest import golden
+
+gpu = pytest.mark.gpu
+
+
+def test_pointset_validation_host():
+    with pytest.raises(mx.ShapeMismatch):
+        mx.PointSet(np.zeros((0, 3), np.float32))
+    with pytest.raises(mx.ShapeMismatch):
+        mx.PointSet(np.zeros(3, np.float32))
+    with pytest.raises(mx.NaNInput):
+        mx.PointSet([[0.0, np.inf, 0.0]])
+
+
+@gpu
+def test_hand_case_and_ties():
+    g = golden("chamfer")
+    cd, a1, a2 = mx.chamfer_forward(g["h_p"], g["h_s"])
+    assert cd == 3.5 == float(g["h_cd"])
+    assert a1.cpu().tolist() == [0] and a2.cpu().tolist() == [0, 0]
+    cd, a1, a2 = mx.chamfer_forward(g["tp"], g["ts"])
+    assert cd == float(g["cdt"])
+    assert np.array_equal(a1.cpu().numpy(), g["t1"]) and np.array_equal(a2.cpu().numpy(), g["t2"])
+    p = mx.PointSet(g["p"][:40])
+    cd, a1, a2 = mx.chamfer_forward(p, p)
+    assert cd == 0.0 and np.array_equal(a1.cpu().numpy(), np.arange(40))
+
+
+@gpu
+@pytest.mark.parametrize("suffix", ["", "5"])
+def test_forward_backward_bit_exact_with_reference(suffix):
+    g = golden("chamfer")
+    p, s = g["p" + suffix], g["s" + suffix]
+    cd, a1, a2 = mx.chamfer_forward(p, s)
+    assert cd == float(g["cd" + suffix])
+    n1, n2 = ("a1", "a2") if not suffix else ("b1", "b2")
+    assert np.array_equal(a1.cpu().numpy(), g[n1]) and np.array_equal(a2.cpu().numpy(), g[n2])
+    up = 1.7 if not suffix else 1.0
+    d_p, d_s = mx.chamfer_backward(p, s, a1, a2, upstream=up)
+    assert np.array_equal(d_p.cpu().numpy(), g["dp" + suffix]) and np.array_equal(d_s.cpu().numpy(), g["ds" + suffix])
+    # the dense reference paths agree (f64 oracle to tolerance, f32 path bit-identical)
+    assert mx.dense_chamfer_forward(p, s)[0] == cd
+    assert mx.dense_chamfer_forward(p, s, precision="f64")[0] == pytest.approx(cd, rel=1e-5)
+    r_p, r_s = mx.dense_chamfer_backward(p, s, a1, a2, upstream=up)
+    assert torch.allclose(d_p, r_p, rtol=1e-12, atol=0) and torch.allclose(d_s, r_s, rtol=1e-12, atol=0)
+
+
+@gpu
+def test_errors():
+    g = golden("chamfer")
+    with pytest.raises(mx.DimMismatch):
+        mx.chamfer_forward(g["p"], g["p5"])
+    _, a1, a2 = mx.chamfer_forward(g["p"], g["s"])
+    with pytest.raises(mx.StaleArgmin):
+        mx.chamfer_backward(g["p"], g["s"], a1[:-1], a2)
+    bad = a1.clone()
+    bad[0] = 10_000
+    with pytest.raises(mx.StaleArgmin):
+        mx.chamfer_backward(g["p"], g["s"], bad, a2)
+    d_p, d_s = mx.chamfer_backward(g["p"], g["s"], a1, a2, upstream=0.0)
+    assert not bool(d_p.any()) and not bool(d_s.any())
+
+
+@gpu
+def test_large_cloud_against_f64_oracle():
+    rng = np.random.default_rng(31)
+    p = rng.standard_normal((20_000, 3)).astype(np.float32)
+    s = rng.standard_normal((30_000, 3)).astype(np.float32)
+    cd, a1, a2 = mx.chamfer_forward(p, s)
+    # f64 nearest neighbours on a subsample of rows
+    P, S = torch.from_numpy(p).cuda().double(), torch.from_numpy(s).cuda().double()
+    rows = torch.arange(0, 20_000, 97, device="cuda")
+    d = ((P[rows, None, :] - S[None, :, :]) ** 2).sum(-1)
+    best = d.min(dim=1).values
+    got = ((P[rows] - S[a1[rows].long()]) ** 2).sum(-1)
+    assert torch.allclose(got, best, rtol=1e-4, atol=1e-6)
+    d_p, d_s = mx.chamfer_backward(p, s, a1, a2)
+    assert d_p.shape == (20_000, 3) and d_s.shape == (30_000, 3)
