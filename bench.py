@@ -357,10 +357,12 @@ def run_ours(a, rank, world, local_rank):
     achieved = flops_per_launch / avg_fwd_s / 1e12
     peak = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "fwd_c2_ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r1_ncu_fwd.json")  # ncu --set full of this kernel at this shape
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            pj = json.load(fh)
+        if pj.get("dram_bytes_read") is not None:
+            traffic = pj["dram_bytes_read"] + (pj.get("dram_bytes_write") or 0.0)
     value = world * nb * a.steps / (max_ms / 1e3)
     line = {
         "metric": METRIC,
@@ -385,6 +387,8 @@ def run_ours(a, rank, world, local_rank):
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_src})",
             "unit": "TFLOP/s",
             "frac": achieved / peak,
+            "frac_vs_sustained_peak": achieved / float(peaks.get("bf16_tflops_sustained",
+                                                               PEAKS_FALLBACK["bf16_tflops_sustained"])),
             "traffic": traffic,
             "flops_per_launch": flops_per_launch,
             "avg_launch_ms": avg_fwd_s * 1e3,
