@@ -122,6 +122,10 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
       if (base + j >= vl) v[j] = -INFINITY;
   }
   const float cmax = max32(v);
+  if (stash_row == nullptr) {  // scores only (argmax not requested): the running max is all
+    m = fmaxf(m, cmax);
+    return;
+  }
   const bool upd = cmax > m;
   if (__any_sync(0xffffffffu, upd)) {
     if (upd) {
@@ -386,7 +390,8 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           sph ^= 1u;
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kTsAccCol0 + slot * 128);
-          float* stash = sBest + ((size_t)mb * 128 + row_local) * 32;
+          // argmax not requested (rerank: scores only) -> no index tracking at all
+          float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * 32 : nullptr;
           const int base = t * kTileRows;
           if (p.debug == 2) {  // profiling knob: drain the slot without folding
             tc_fence_before();

@@ -388,6 +388,18 @@ def test_training_drift_matches_reference_loop():
     assert drift <= 1e-4
 
 
+def test_scores_without_argmax_are_identical():
+    """The rerank mode (argmax not requested: max only, no index tracking) returns the same bits."""
+    rng = np.random.default_rng(17)
+    Q = cuda(orc.make_queries(2, 300, 128, seed=3), torch.bfloat16)
+    lens = rng.integers(1, 400, 37).astype(np.int32)
+    D, vl = orc.padded(orc.make_corpus(37, lens, 128, seed=4), 400)
+    Dt, vlt = cuda(D, torch.bfloat16), cuda(vl)
+    s1, a1, r1 = mx.score_dense(Q, Dt, vlt)
+    s2, a2, r2 = mx.score_dense(Q, Dt, vlt, want_argmax=False)
+    assert a2 is None and torch.equal(s1, s2) and torch.equal(r1, r2)
+
+
 # ------------------------------------------------------------------ top-K (K9)
 def test_topk_ties_and_chunking():
     g = golden("misc")
