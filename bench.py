@@ -469,6 +469,8 @@ def run_e2e(a, Q, D, rank, world, dev, torch, dist):
         "unit": UNIT,
         "h2d_bytes_per_step": int(Q.numel() * 2 + D.numel() * 2),
         "d2h_bytes_per_step": int(a.docs * 8 + a.topk * 8),
+        "h2d_gbps_effective": (Q.numel() * 2 + D.numel() * 2) * steps / (float(ms.item()) / 1e3) / 1e9,
+        "bound": "host-to-device link (each step re-sends the 2.62 GB bf16 corpus from pinned memory)",
         "steps": steps,
         "path": "paper_2605_29517_b200.score_dense + topk (public API), pinned host buffers",
     }

@@ -89,7 +89,8 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     Q [N_q, L_q, d] replicated; D_local [B/W, L, d] this rank's documents starting at global
     doc `doc_offset`.  Returns (loss, scores [N_q, B], dQ [N_q, L_q, d] fp32 all-reduced,
     dD_local [B/W, L, d] fp32).  Collectives: one all_gather of the local score blocks, one
-    all_reduce(sum) of dQ; dD never leaves its rank.
+    all_reduce(sum) of dQ issued asynchronously and overlapped with the dD kernel; dD never
+    leaves its rank.
     """
     import torch.distributed as dist
 
@@ -104,8 +105,10 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     loss, g_full = softmax_ce(scores)
     b_local, l_pad, dim = D_local.shape
     g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
-    dD = kernels.grad_docs(Q.to(D_local.dtype).contiguous(), argmax, g, l_pad)
+    # dQ first: its all_reduce (NCCL, async) crosses NVLink while the dD gather kernel runs
     dQ = kernels.grad_query(D_local, argmax, g)
-    if world > 1:
-        dist.all_reduce(dQ, group=group)
+    work = dist.all_reduce(dQ, group=group, async_op=True) if world > 1 else None
+    dD = kernels.grad_docs(Q.to(D_local.dtype).contiguous(), argmax, g, l_pad)
+    if work is not None:
+        work.wait()
     return loss, scores, dQ, dD.reshape(b_local, l_pad, dim)

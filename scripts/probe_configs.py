@@ -42,9 +42,12 @@ Qf = unit(1, 1024, 128); Df = torch.empty(nb, 1024, 128, dtype=torch.bfloat16, d
 for i in range(0, nb, 1000): Df[i:i + 1000] = unit(1000, 1024, 128)
 t_q = timeit(lambda: mx.quant.quantize_tensor(Df))
 dq, ds = mx.quant.quantize_tensor(Df); qq, qs = mx.quant.quantize_tensor(Qf)
-t_i8 = timeit(lambda: mx.score_int8(qq, qs, dq, ds))
-t_bf = timeit(lambda: mx.score_dense(Qf, Df))
-print(f"C4 int8 {t_i8:.3f} ms ({nb / t_i8 * 1e3 / 1e6:.2f} M docs/s, {2.684e12 / t_i8 / 1e9:.0f} TOP/s) | bf16 {t_bf:.3f} ms | quantize corpus {t_q:.3f} ms")
+t_i8 = timeit(lambda: mx.score_int8(qq, qs, dq, ds, want_argmax=False))
+t_i8a = timeit(lambda: mx.score_int8(qq, qs, dq, ds))
+t_bf = timeit(lambda: mx.score_dense(Qf, Df, want_argmax=False))
+t_bfa = timeit(lambda: mx.score_dense(Qf, Df))
+print(f"C4 int8 rerank {t_i8:.3f} ms ({nb / t_i8 * 1e3 / 1e6:.2f} M docs/s, {2.684e12 / t_i8 / 1e9:.0f} TOP/s), "
+      f"+argmax {t_i8a:.3f} ms | bf16 rerank {t_bf:.3f} ms, +argmax {t_bfa:.3f} ms | quantize corpus {t_q:.3f} ms")
 del Df, dq
 
 # C5 scaled: varlen 100K docs L in [32, 512], L_q = 32
@@ -56,9 +59,10 @@ T = int(cu[-1])
 toks = torch.empty(T, 128, dtype=torch.bfloat16, device="cuda")
 for i in range(0, T, 4_000_000): toks[i:i + 4_000_000] = unit(min(4_000_000, T - i), 128)
 q5 = unit(1, 32, 128)
-t_v = timeit(lambda: mx.score_varlen(q5, toks, cu), reps=3, warm=1)
+t_v = timeit(lambda: mx.score_varlen(q5, toks, cu, want_argmax=False), reps=3, warm=1)
+t_va = timeit(lambda: mx.score_varlen(q5, toks, cu), reps=3, warm=1)
 byt = T * 256
-print(f"C5 varlen {n5} docs ({T} tokens): {t_v:.3f} ms ({n5 / t_v * 1e3 / 1e6:.2f} M docs/s, {byt / t_v / 1e6:.0f} GB/s)")
+print(f"C5 varlen {n5} docs ({T} tokens): rerank {t_v:.3f} ms ({n5 / t_v * 1e3 / 1e6:.2f} M docs/s, {byt / t_v / 1e6:.0f} GB/s), +argmax {t_va:.3f} ms")
 sc, _, _ = mx.score_varlen(q5, toks, cu)
 t_k = timeit(lambda: mx.topk(sc[0], 20))
 print(f"topk 20 of {n5}: {t_k:.3f} ms")
