@@ -136,6 +136,45 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
   }
 }
 
+// Fast path of ts_chunk for a chunk that lies entirely inside the document (no masking), with
+// the INT8 scales already in shared memory and the argmax decision made at compile time: no
+// per-chunk bounds checks or pointer tests, so the compiler sees one straight-line block.
+template <TcKind KIND, bool kArgmax>
+MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m, int& cb, float* stash_row, int swz,
+                           const float* sd_smem) {
+  float v[32];
+  if constexpr (KIND == TcKind::I8) {
+    const float4* s4 = reinterpret_cast<const float4*>(sd_smem);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 t = s4[c];
+      float c0, c1, c2, c3, t0, t1, t2, t3;
+      i2f2_magic(c0, c1, r[4 * c], r[4 * c + 1]);
+      i2f2_magic(c2, c3, r[4 * c + 2], r[4 * c + 3]);
+      fmul2_rn(t0, t1, c0, c1, sq, sq);
+      fmul2_rn(t2, t3, c2, c3, sq, sq);
+      fmul2_rn(v[4 * c], v[4 * c + 1], t0, t1, t.x, t.y);
+      fmul2_rn(v[4 * c + 2], v[4 * c + 3], t2, t3, t.z, t.w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  }
+  const float cmax = max32(v);
+  if constexpr (!kArgmax) {
+    m = fmaxf(m, cmax);
+  } else {
+    const bool upd = cmax > m;
+    if (__any_sync(0xffffffffu, upd)) {
+      if (upd) {
+        m = cmax;
+        cb = base;
+        stash_chunk(stash_row, v, swz);
+      }
+    }
+  }
+}
+
 template <TcKind KIND, int KA, int CL>
 __global__ void __launch_bounds__(kTsThreads, 1)
     fwd_ts_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
@@ -397,6 +436,32 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+          } else if (KIND == TcKind::I8 && KA <= 2 && sdt != nullptr && base + kTileRows <= vl) {
+            // full tile, staged scales: straight-line chunks, argmax tracking decided at compile time
+            uint32_t ra[32], rb[32];
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tmem_ld_wait();
+            if (stash) {
+              ts_chunk_full<KIND, true>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
+              ts_chunk_full<KIND, true>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
+            } else {
+              ts_chunk_full<KIND, false>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
+              ts_chunk_full<KIND, false>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
+            }
+            tmem_ld32(taddr + 64, ra);
+            tmem_ld32(taddr + 96, rb);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+            if (stash) {
+              ts_chunk_full<KIND, true>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
+              ts_chunk_full<KIND, true>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
+            } else {
+              ts_chunk_full<KIND, false>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
+              ts_chunk_full<KIND, false>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
+            }
           } else if constexpr (KIND == TcKind::I8) {
             // the dequantisation needs extra registers: two chunks in flight at a time
             uint32_t ra[32], rb[32];
@@ -413,6 +478,27 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
             ts_chunk<KIND, (KA <= 2)>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 64 : sdt);
             ts_chunk<KIND, (KA <= 2)>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 96 : sdt);
+          } else if (KIND != TcKind::I8 && base + kTileRows <= vl) {
+            uint32_t ra[32], rb[32], rc[32], rd[32];
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tmem_ld32(taddr + 64, rc);
+            tmem_ld32(taddr + 96, rd);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+            if (stash) {
+              ts_chunk_full<KIND, true>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
+            } else {
+              ts_chunk_full<KIND, false>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
+            }
           } else {
             uint32_t ra[32], rb[32], rc[32], rd[32];
             tmem_ld32(taddr, ra);

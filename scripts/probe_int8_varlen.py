@@ -14,7 +14,7 @@ if which in ("both", "int8"):
     qq, qs = mx.quant.quantize_tensor(unit(1, 1024, 128))
     dq, ds = mx.quant.quantize_tensor(unit(nb, 1024, 128))
     for _ in range(3):
-        mx.score_int8(qq, qs, dq, ds)
+        mx.score_int8(qq, qs, dq, ds, want_argmax=os.environ.get("ARGMAX", "1") == "1")
 if which in ("both", "varlen"):
     rng = np.random.default_rng(0)
     lens = rng.integers(32, 513, 50000)
