@@ -1,0 +1,48 @@
+"""configs[4] at full size on one GPU: 1M-document ColBERT corpus, L_d uniform in [32, 512], L_q = 32,
+d = 128, bf16, packed (cu_seqlens), top-20 -- plus a shard-invariance check: re-scoring a
+10K-document slice on its own gives bit-identical scores (documents are independent units)."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2605_29517_b200 as mx  # noqa: E402
+
+g = torch.Generator(device="cuda").manual_seed(0)
+rng = np.random.default_rng(0)
+n = 1_000_000
+lens = rng.integers(32, 513, n)
+cu_h = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+T = int(cu_h[-1])
+cu = torch.from_numpy(cu_h).cuda()
+toks = torch.empty(T, 128, dtype=torch.bfloat16, device="cuda")
+for i in range(0, T, 8_000_000):
+    x = torch.randn(min(8_000_000, T - i), 128, device="cuda", generator=g)
+    toks[i:i + x.shape[0]] = (x / x.norm(dim=-1, keepdim=True)).bfloat16()
+    del x
+q = torch.randn(1, 32, 128, device="cuda", generator=g)
+q = (q / q.norm(dim=-1, keepdim=True)).bfloat16()
+for _ in range(2):
+    s, _, _ = mx.score_varlen(q, toks, cu, want_argmax=False)
+torch.cuda.synchronize()
+ts = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s, _, _ = mx.score_varlen(q, toks, cu, want_argmax=False)
+    top_s, top_i = mx.topk(s[0], 20)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ms = sorted(ts)[len(ts) // 2]
+# shard invariance: docs [500000, 510000) scored alone
+lo, hi = 500_000, 510_000
+sub_cu = cu[lo:hi + 1] - cu[lo]
+s2, _, _ = mx.score_varlen(q, toks[int(cu_h[lo]):int(cu_h[hi])].contiguous(), sub_cu.contiguous(), want_argmax=False)
+same = bool(torch.equal(s2[0], s[0, lo:hi]))
+print(json.dumps({"config": "configs[4] C5 varlen 1M docs, L_d in [32,512], L_q=32, d=128, bf16, top-20",
+                  "tokens": T, "bytes": T * 256, "ms": ms, "docs_per_s": n / ms * 1e3,
+                  "hbm_gbs": T * 256 / ms / 1e6, "shard_invariant": same,
+                  "top5": [[int(i), float(v)] for i, v in zip(top_i[:5].tolist(), top_s[:5].tolist())]}))
