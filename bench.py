@@ -437,17 +437,16 @@ def run_e2e(a, Q, D, rank, world, dev, torch, dist):
     out_s = torch.empty((1, a.docs), dtype=torch.float64, pin_memory=True)
     out_t = torch.empty(a.topk, dtype=torch.int64, pin_memory=True)
     dq = torch.empty_like(Q)
-    dd = torch.empty_like(D)
     stream = torch.cuda.current_stream()
     steps = max(1, min(a.steps, 5))
 
     def one():
+        # public API for a host-resident corpus: block i+1 crosses the host link while block i
+        # is scored (query copied too); results (all scores + top-K ids) read back to the host
         dq.copy_(hq, non_blocking=True)
-        dd.copy_(hd, non_blocking=True)
-        scores, _, _ = mx.score_dense(dq, dd, want_argmax=False)
-        ts, ti = mx.topk(scores[0], a.topk, id_offset=rank * a.docs)
-        out_s.copy_(scores, non_blocking=True)
-        out_t.copy_(ti, non_blocking=True)
+        scores, ts, ti = mx.stream_score_host(dq[0], hd, k=a.topk, block_docs=1000)
+        out_s[0].copy_(scores, non_blocking=True)
+        out_t.copy_(ti + rank * a.docs, non_blocking=True)
 
     one()
     torch.cuda.synchronize()
@@ -463,7 +462,7 @@ def run_e2e(a, Q, D, rank, world, dev, torch, dist):
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    del hd, dd
+    del hd
     return {
         "value": world * a.docs * steps / (float(ms.item()) / 1e3),
         "unit": UNIT,
@@ -472,7 +471,8 @@ def run_e2e(a, Q, D, rank, world, dev, torch, dist):
         "h2d_gbps_effective": (Q.numel() * 2 + D.numel() * 2) * steps / (float(ms.item()) / 1e3) / 1e9,
         "bound": "host-to-device link (each step re-sends the 2.62 GB bf16 corpus from pinned memory)",
         "steps": steps,
-        "path": "paper_2605_29517_b200.score_dense + topk (public API), pinned host buffers",
+        "path": "paper_2605_29517_b200.stream_score_host (public API): pinned host corpus, H2D of block i+1 "
+                "overlapped with the scoring of block i, device top-K merge",
     }
 
 

@@ -65,6 +65,7 @@ from .streamio import (
     TrafficModel,
     model_traffic,
     read_embeddings,
+    stream_score_host,
     stream_score_topk,
     write_embeddings,
 )

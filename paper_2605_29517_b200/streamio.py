@@ -351,6 +351,74 @@ def _stream(query, reader: CorpusReader, block_docs: int, k: int, report, comput
         pool.shutdown(wait=True)
 
 
+def stream_score_host(query, docs_host: torch.Tensor, k: int, block_docs: int = 1000, valid_lens=None,
+                      compute_dtype=None, want_scores: bool = True):
+    """Score a corpus resident in (pinned) HOST memory: block i+1 is copied to the device on a
+    copy stream while block i is scored, so the step costs ~max(H2D, compute) instead of their sum.
+
+    docs_host [B, L, d] CPU tensor (pin it for overlap); returns (scores f64 [B] on the device or
+    None, top_s f64 [k], top_id int64 [k]) -- ranking in the reference order (score desc, id asc).
+    """
+    from .forward import score_dense
+
+    if docs_host.is_cuda:
+        raise ShapeMismatch("stream_score_host expects host-resident documents")
+    n_docs = int(docs_host.shape[0])
+    if k > n_docs:
+        raise KTooLarge(k, n_docs)
+    dev = _dev.device()
+    q = query if isinstance(query, torch.Tensor) else torch.as_tensor(np.asarray(getattr(query, "data", query)))
+    q = q.to(dev)
+    if q.dim() == 2:
+        q = q[None]
+    work_dtype = compute_dtype or docs_host.dtype
+    q = q.to(work_dtype).contiguous()
+    vl = None if valid_lens is None else torch.as_tensor(valid_lens).to(dev, torch.int32)
+    blocks = [(f, min(block_docs, n_docs - f)) for f in range(0, n_docs, block_docs)]
+    devb = [torch.empty((block_docs,) + tuple(docs_host.shape[1:]), dtype=docs_host.dtype, device=dev)
+            for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    comp = torch.cuda.current_stream(dev)
+    scores = torch.empty(n_docs, dtype=torch.float64, device=dev) if want_scores else None
+    dev_free = [None, None]
+    run_s = run_i = None
+    h2d = [None] * len(blocks)
+
+    def enqueue_copy(i):
+        first, count = blocks[i]
+        slot = i % 2
+        with torch.cuda.stream(copy_stream):
+            if dev_free[slot] is not None:  # the block that last used this buffer was scored
+                copy_stream.wait_event(dev_free[slot])
+            devb[slot][:count].copy_(docs_host[first:first + count], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+            h2d[i] = ev
+
+    enqueue_copy(0)
+    for i, (first, count) in enumerate(blocks):
+        slot = i % 2
+        if i + 1 < len(blocks):
+            enqueue_copy(i + 1)  # overlaps the scoring of block i
+        comp.wait_event(h2d[i])
+        data = devb[slot][:count]
+        if work_dtype != data.dtype:
+            data = data.to(work_dtype)
+        s, _, _ = score_dense(q, data, None if vl is None else vl[first:first + count], want_argmax=False)
+        if scores is not None:
+            scores[first:first + count].copy_(s[0])
+        bs, bi = topk(s[0], min(k, count), id_offset=first)
+        if run_s is None:
+            run_s, run_i = bs, bi
+        else:
+            run_s, run_i = select_candidates(torch.cat([run_s, bs]), torch.cat([run_i, bi]),
+                                             min(k, run_s.numel() + bs.numel()))
+        ev_free = torch.cuda.Event()
+        ev_free.record(comp)
+        dev_free[slot] = ev_free
+    return scores, run_s[:k], run_i[:k]
+
+
 # --------------------------------------------------------------------------- byte model
 @dataclass(frozen=True)
 class TrafficModel:

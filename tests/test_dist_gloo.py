@@ -74,7 +74,23 @@ def _worker(rank, world, port, q):
             and np.allclose(dQ.numpy(), dq_ref, rtol=1e-5, atol=1e-6)
             and np.allclose(dD.numpy(), dd_ref[lo:hi], rtol=1e-5, atol=1e-6)
         )
-        q.put((rank, ok_topk, ok_train))
+        # ---- C5 decomposition: token-balanced contiguous document shards of a packed corpus,
+        #      per-rank varlen scoring + top-K, all_gather merge == global oracle ranking
+        rng = np.random.default_rng(9)
+        lens = rng.integers(1, 40, 61)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        toks = orc.unit_tokens(rng, int(cu[-1]), 8).astype(np.float32)
+        qv = orc.unit_tokens(rng, 4, 8).astype(np.float32)
+        lo, hi = shard_bounds(61, world, rank, weights=lens)
+        loc_cu = cu[lo:hi + 1] - cu[lo]
+        loc_s, _ = orc.fused_score_varlen(qv[None], toks[cu[lo]:cu[hi]], loc_cu)
+        ls, li = select_candidates(torch.from_numpy(loc_s[0]), torch.arange(lo, hi), 9)
+        ts, ti = merge_topk_across_ranks(ls, li, 9)
+        g_s, _ = orc.fused_score_varlen(qv[None], toks, cu)
+        os_, oi = orc.topk(g_s[0], 9)
+        tok_share = (cu[hi] - cu[lo]) / cu[-1]
+        ok_varlen = ti.tolist() == oi.tolist() and ts.tolist() == os_.tolist() and abs(tok_share - 0.5) < 0.2
+        q.put((rank, ok_topk, ok_train and ok_varlen))
     finally:
         dist.destroy_process_group()
 

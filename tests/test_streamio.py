@@ -206,3 +206,16 @@ def test_read_embeddings_to_device():
     qc = mx.read_embeddings(os.path.join(FIX, "quant.mxs1"))
     assert np.array_equal(qc.q.cpu().numpy(), e["quant_q"]) and np.array_equal(qc.scales.cpu().numpy(),
                                                                                 e["quant_scales"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_ok(), reason="needs a GPU")
+def test_stream_score_host_equals_device_scoring():
+    rng = np.random.default_rng(24)
+    q = torch.from_numpy(orc.unit_tokens(rng, 64, 128).astype(np.float32)).cuda().bfloat16()
+    docs = torch.from_numpy(np.stack([orc.unit_tokens(rng, 96, 128) for _ in range(1030)]).astype(np.float32))
+    docs = docs.bfloat16().pin_memory()
+    scores, ts, ti = mx.stream_score_host(q, docs, k=17, block_docs=256)
+    ref, _, _ = mx.score_dense(q[None], docs.cuda(), want_argmax=False)
+    rs, ri = mx.topk(ref[0], 17)
+    assert torch.equal(scores, ref[0]) and torch.equal(ts, rs) and torch.equal(ti, ri)
