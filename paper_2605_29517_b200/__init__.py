@@ -59,6 +59,7 @@ from .quant import (
 from .varlen import PackedCorpus, fused_score_varlen, pack, score_varlen, unpack
 from .topk import TopKHeap, ranked, topk
 from .autograd import MaxSimFunction, MaxSimVarlenFunction, maxsim, maxsim_varlen
+from .training import contrastive_drift, softmax_ce
 from .chamfer import PointSet, chamfer_backward, chamfer_forward, dense_chamfer_backward, dense_chamfer_forward
 from .streamio import (
     CorpusReader,

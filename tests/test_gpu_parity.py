@@ -388,6 +388,13 @@ def test_training_drift_matches_reference_loop():
     assert drift <= 1e-4
 
 
+def test_contrastive_drift_api():
+    """maxsim/cli.py:209 contrastive_drift on the device: fused path vs dense path."""
+    out = mx.contrastive_drift(n_docs=4, len_q=6, len_d=7, dim=8, steps=40, seed=3)
+    assert out["steps"] == 40 and out["max_rel_drift"] <= 1e-4
+    assert out["loss_last_fused"] < out["loss_first"]
+
+
 def test_scores_without_argmax_are_identical():
     """The rerank mode (argmax not requested: max only, no index tracking) returns the same bits."""
     rng = np.random.default_rng(17)
