@@ -244,8 +244,8 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
                      int64_t n_tokens, int64_t dim, float* rowmax, int32_t* argmax, cudaStream_t st) {
   static_assert(KIND != mxs::TcKind::I8, "varlen is a bf16 / f16 path");
   const int eb = 2;
-  const long long n_cols = n_q * l_q;
-  if (n_cols > 128 || (dim * eb) % 16 != 0) return MXS_UNSUPPORTED;
+  const long long rows = n_q * l_q;
+  if ((dim * eb) % 16 != 0 || rows >= (1LL << 31)) return MXS_UNSUPPORTED;
   const int ka = (int)((dim * eb + 127) / 128);
   if (ka > 4) return MXS_UNSUPPORTED;
   const size_t max_smem = 232448 - sizeof(mxs::VrSmemHeader);
@@ -253,26 +253,6 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
-  mxs::VarlenRowsParams p = {};
-  p.n_q = (int)n_q;
-  p.l_q = (int)l_q;
-  p.n_cols = (int)n_cols;
-  p.copies = n_cols <= 32 ? 4 : (n_cols <= 64 ? 2 : 1);  // query-row replication over TMEM quadrants
-  p.n_docs = n_docs;
-  p.n_tokens = n_tokens;
-  p.dim = (int)dim;
-  p.stages = stages;
-  p.cu = (const long long*)cu;
-  p.rowmax = rowmax;
-  p.argmax = argmax;
-  const CUtensorMapDataType dt =
-      (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap tt, tq;
-  int s;
-  if ((s = make_tmap_2d(&tt, tokens, dt, eb, dim, n_tokens)) != MXS_OK) return s;
-  // one box per row copy; rows >= n_cols read as 0
-  if ((s = make_tmap_2d(&tq, Q, dt, eb, dim, n_cols, 128 / p.copies)) != MXS_OK) return s;
-  const size_t smem = mxs::varlen_rows_smem_bytes(ka, stages);
   void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::VarlenRowsParams) = nullptr;
   switch (ka) {
     case 1: kern = mxs::varlen_rows_kernel<KIND, 1>; break;
@@ -281,13 +261,42 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
     case 4: kern = mxs::varlen_rows_kernel<KIND, 4>; break;
     default: return MXS_UNSUPPORTED;
   }
+  const size_t smem = mxs::varlen_rows_smem_bytes(ka, stages);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
   const int nsm = sm_count();
   if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
   const long long grid = n_docs < nsm ? n_docs : nsm;
-  kern<<<(unsigned)grid, mxs::kVrThreads, smem, st>>>(tt, tq, p);
-  return check_launch("varlen_rows_kernel");
+  const CUtensorMapDataType dt =
+      (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tt;
+  int s;
+  if ((s = make_tmap_2d(&tt, tokens, dt, eb, dim, n_tokens)) != MXS_OK) return s;
+  // More than 128 query rows (e.g. ColPali queries): one launch per 128-row group; every group
+  // streams the token corpus once and writes its own (q, i) outputs.
+  for (long long row0 = 0; row0 < rows; row0 += 128) {
+    const long long n_cols = std::min(128LL, rows - row0);
+    mxs::VarlenRowsParams p = {};
+    p.n_q = (int)n_q;
+    p.l_q = (int)l_q;
+    p.n_cols = (int)n_cols;
+    p.row0 = (int)row0;
+    p.copies = n_cols <= 32 ? 4 : (n_cols <= 64 ? 2 : 1);  // query-row replication over TMEM quadrants
+    p.n_docs = n_docs;
+    p.n_tokens = n_tokens;
+    p.dim = (int)dim;
+    p.stages = stages;
+    p.cu = (const long long*)cu;
+    p.rowmax = rowmax;
+    p.argmax = argmax;
+    CUtensorMap tq;
+    const void* q0 = static_cast<const uint8_t*>(Q) + row0 * dim * eb;
+    // one box per row copy; rows >= n_cols read as 0
+    if ((s = make_tmap_2d(&tq, q0, dt, eb, dim, n_cols, 128 / p.copies)) != MXS_OK) return s;
+    kern<<<(unsigned)grid, mxs::kVrThreads, smem, st>>>(tt, tq, p);
+    if ((s = check_launch("varlen_rows_kernel")) != MXS_OK) return s;
+  }
+  return MXS_OK;
 }
 
 bool use_ts_path() {

@@ -24,7 +24,8 @@
 namespace mxs {
 
 struct VarlenRowsParams {
-  int n_q, l_q, n_cols;  // n_cols = n_q * l_q <= 128 query rows
+  int n_q, l_q, n_cols;  // this launch: flattened query rows [row0, row0 + n_cols), n_cols <= 128
+  int row0;
   int copies;            // row replication C (4, 2 or 1)
   long long n_docs, n_tokens;
   int dim;
@@ -90,7 +91,8 @@ MXS_DEV long long vr_doc_of_token(const long long* cu, long long lo, long long h
 // output offset of (query row, document 0); rows >= n_cols get -1 (nothing is written)
 MXS_DEV long long vr_row_base(const VarlenRowsParams& p, int row) {
   if (row >= p.n_cols) return -1;
-  const int q = row / p.l_q, i = row - q * p.l_q;
+  const int r = p.row0 + row;
+  const int q = r / p.l_q, i = r - q * p.l_q;
   return (long long)q * p.n_docs * p.l_q + i;
 }
 MXS_DEV void vr_emit(const VarlenRowsParams& p, long long rbase, long long doc, float m, long long arg_local) {

@@ -455,11 +455,12 @@ def test_sharded_rerank_merge_equals_global():
 @pytest.mark.parametrize(
     "n_docs,lo,hi,l_q,n_q",
     [(300, 32, 512, 32, 1), (1000, 1, 20, 32, 1), (50, 100, 2000, 32, 1), (200, 1, 300, 16, 4), (100, 5, 200, 128, 1),
-     (7, 1, 3, 32, 1)],
+     (7, 1, 3, 32, 1), (40, 5, 300, 48, 3), (30, 10, 100, 100, 3), (24, 50, 700, 1024, 1)],
 )
 def test_varlen_tensor_core_vs_exact_and_oracle(n_docs, lo, hi, l_q, n_q):
     """K5 (tcgen05 varlen): documents start/end anywhere in a 128-token tile, 1-token docs, docs
-    spanning many tiles, multi-query column blocks; vs the exact kernel and the oracle."""
+    spanning many tiles, multi-query column blocks, more than 128 query rows (one launch per
+    128-row group, a query split across groups); vs the exact kernel and the oracle."""
     rng = np.random.default_rng(n_docs + l_q)
     lens = rng.integers(lo, hi + 1, n_docs)
     cu = np.concatenate([[0], np.cumsum(lens)])
