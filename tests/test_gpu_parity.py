@@ -192,7 +192,8 @@ def test_int8_golden_bitwise():
     assert s == g["scores"][1] and a.cpu().tolist() == list(g["argmax"][1])
 
 
-@pytest.mark.parametrize("l_q,n_docs,l_pad,dim", [(1024, 12, 1024, 128), (33, 40, 200, 64), (300, 9, 517, 256)])
+@pytest.mark.parametrize("l_q,n_docs,l_pad,dim", [(1024, 12, 1024, 128), (33, 40, 200, 64), (300, 9, 517, 256),
+                                                 (256, 30, 640, 128)])
 def test_int8_random_bitwise_incl_ties(l_q, n_docs, l_pad, dim):
     rng = np.random.default_rng(l_q + dim)
     Qf = rng.standard_normal((2, l_q, dim)).astype(np.float32)
@@ -209,6 +210,9 @@ def test_int8_random_bitwise_incl_ties(l_q, n_docs, l_pad, dim):
                                         ds_o.reshape(n_docs, l_pad), lens)
     assert np.array_equal(sc.cpu().numpy(), ref_s)
     assert np.array_equal(am.cpu().numpy(), ref_a)
+    # rerank mode (no argmax, max-only fast path): the same bits
+    sc2, am2, _ = mx.score_int8(qq, qs, dq, ds, cuda(lens.astype(np.int32)), want_argmax=False)
+    assert am2 is None and np.array_equal(sc2.cpu().numpy(), ref_s)
 
 
 def test_two_stage_topk_matches_reference():
