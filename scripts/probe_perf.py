@@ -23,9 +23,12 @@ def P(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+WANT_ARGMAX = os.environ.get("ARGMAX", "1") == "1"
+
+
 def go():
-    _lib.call("mxs_fused_score_batch", _lib.MXS_BF16, P(Q), 1, lq, P(D), nb, 1024, 128, None, P(scores), P(am),
-              P(rm), 0, st)
+    _lib.call("mxs_fused_score_batch", _lib.MXS_BF16, P(Q), 1, lq, P(D), nb, 1024, 128, None, P(scores),
+              P(am) if WANT_ARGMAX else None, P(rm), 0, st)
 
 
 for _ in range(3):
@@ -41,4 +44,5 @@ for _ in range(int(os.environ.get("REPS", "10"))):
     ts.append(e0.elapsed_time(e1))
 t = sorted(ts)[len(ts) // 2]
 fl = 2 * lq * 1024 * 128 * nb
-print(f"debug={os.environ.get('MXS_DEBUG', '0')} nb={nb} lq={lq}: {t:.3f} ms {fl / t / 1e9:.0f} TFLOP/s")
+print(f"debug={os.environ.get('MXS_DEBUG', '0')} argmax={int(WANT_ARGMAX)} nb={nb} lq={lq}: {t:.3f} ms "
+      f"{fl / t / 1e9:.0f} TFLOP/s")
