@@ -12,6 +12,7 @@
 #include "fwd_exact.cuh"
 #include "fwd_tc.cuh"
 #include "fwd_ts.cuh"
+#include "fwd_i8r.cuh"
 #include "varlen_rows.cuh"
 #include "csr.cuh"
 #include "grad.cuh"
@@ -156,6 +157,72 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   if (grid <= 0) return MXS_OK;
   kern<<<(unsigned)grid, mxs::kFwdThreads, smem, st>>>(tq, td, p);
   return check_launch("fwd_tc_kernel");
+}
+
+// INT8 rerank path (argmax not requested, d <= 128): three epilogue warp sets (fwd_i8r.cuh).
+// Returns MXS_UNSUPPORTED (without launching) otherwise.
+int launch_fwd_i8r(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad,
+                   int64_t dim, const int32_t* valid_lens, const float* q_scale, const float* d_scale, float* rowmax,
+                   cudaStream_t st) {
+  if (dim % 16 != 0 || dim > 128 || l_pad % 4 != 0) return MXS_UNSUPPORTED;
+  {
+    const char* impl = getenv("MXS_I8_IMPL");
+    if (impl && strcmp(impl, "ts") == 0) return MXS_UNSUPPORTED;
+  }
+  const int nmb = (int)((l_q + 127) / 128);
+  const int qb = std::min(mxs::kMaxQb, nmb);
+  const int n_groups = (nmb + qb - 1) / qb;
+  const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
+  const size_t max_smem = 232448 - sizeof(mxs::R8SmemHeader);
+  const size_t fixed = mxs::fwd_i8r_smem_bytes(0);
+  int stages = (int)((max_smem - fixed) / (size_t)mxs::kAtomBytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return MXS_UNSUPPORTED;
+  mxs::FwdTcParams p = {};
+  p.n_q = (int)n_q;
+  p.l_q = (int)l_q;
+  p.n_docs = (int)n_docs;
+  p.l_pad = (int)l_pad;
+  p.dim = (int)dim;
+  p.ka = 1;
+  p.qb = qb;
+  p.n_groups = n_groups;
+  p.stages = stages;
+  p.n_units = (cl > 1) ? (long long)n_q * n_docs : (long long)n_q * n_groups * n_docs;
+  p.valid_lens = valid_lens;
+  p.q_scale = q_scale;
+  p.d_scale = d_scale;
+  p.rowmax = rowmax;
+  p.argmax = nullptr;
+  p.q_ptr = Q;
+  CUtensorMap td;
+  int s;
+  if ((s = make_tmap_2d(&td, D, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
+  const size_t smem = mxs::fwd_i8r_smem_bytes(stages);
+  using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
+  KernT kern = cl == 4 ? mxs::fwd_i8r_kernel<4> : (cl == 2 ? mxs::fwd_i8r_kernel<2> : mxs::fwd_i8r_kernel<1>);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
+  const int nsm = sm_count();
+  if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
+  long long workers = nsm / cl;
+  if (p.n_units < workers) workers = p.n_units;
+  if (workers <= 0) return MXS_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(workers * cl));
+  cfg.blockDim = dim3(mxs::kR8Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, td, p);
+  if (e != cudaSuccess) return fail(MXS_CUDA_ERROR, "fwd_i8r_kernel launch: %s", cudaGetErrorString(e));
+  return check_launch("fwd_i8r_kernel");
 }
 
 // v3 path: Q in TMEM, cluster multicast of document tiles, stash-based argmax.
@@ -485,7 +552,10 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
     return fail(MXS_SHAPE_MISMATCH, "mxs_fused_score_int8: non-positive shape");
   if (dim > 133000) return fail(MXS_SHAPE_MISMATCH, "dim %lld exceeds 133000 (int32 accumulation bound)", (long long)dim);
   cudaStream_t st = (cudaStream_t)stream;
-  int s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale,
+  int s = argmax ? MXS_UNSUPPORTED
+                 : launch_fwd_i8r(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale, rowmax, st);
+  if (s == MXS_UNSUPPORTED)
+    s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale,
                                                          d_scale, rowmax, argmax, st)
                         : MXS_UNSUPPORTED;
   if (s == MXS_UNSUPPORTED)

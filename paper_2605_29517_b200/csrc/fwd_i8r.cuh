@@ -1,0 +1,319 @@
+// INT8 x INT8 forward, RERANK mode (argmax not requested): scores only -- maxsim/quant.py:128-182
+// with the per-token maxima reduced to the f64 score, no index tracking.
+//
+// The INT8 epilogue is issue-bound (the reference's dequantise-before-max, S7, costs ~3 issued
+// instructions per similarity), so this variant puts THREE epilogue warp sets on the SM instead
+// of two.  Without argmax tracking the running row maximum is order-free (max is exact and
+// commutative), which is what makes the split legal:
+//   * the MMA issuer numbers every (tile, Q block) accumulator it produces, n = 0, 1, 2, ...;
+//     accumulator n lands in TMEM slot n % 3 and is drained by epilogue set n % 3, so each set
+//     consumes its own slot in order (no mbarrier phase aliasing);
+//   * each set keeps, per Q block, a partial maximum over the tiles it happened to drain; at the
+//     end of a document the three partials of every row are max-combined through shared memory
+//     (double-buffered by document parity) and written once.
+// TMEM: 4 Q blocks x 32 columns (d <= 128) + 3 slots x 128 columns = 512.  Everything else
+// (TS MMA with Q resident in TMEM, cluster multicast of document tiles, TMA-staged scales,
+// magic-number s32 -> f32) is fwd_ts.cuh's.
+#pragma once
+#include "fwd_ts.cuh"
+
+namespace mxs {
+
+constexpr int kR8Sets = 3;
+constexpr int kR8EpiWarps = 4 * kR8Sets;
+constexpr int kR8Threads = 32 * (2 + kR8EpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM, 2..13 epilogue
+constexpr int kR8AccCol0 = 128;
+
+struct R8SmemHeader {
+  uint64_t full[8];
+  uint64_t empty[8];
+  uint64_t tfull[kR8Sets];
+  uint64_t tempty[kR8Sets];
+  uint64_t qfull;
+  uint64_t qempty;
+  uint64_t sfull[kScaleSlots];
+  uint64_t sempty[kScaleSlots];
+  uint32_t tmem_base;
+  uint32_t pad;
+};
+
+// dynamic smem: document tiles + per-document partial maxima [2 docs][3 sets][4 blocks][128 rows]
+// + the scale ring
+__host__ __device__ inline size_t fwd_i8r_smem_bytes(int stages) {
+  return 1024 + (size_t)stages * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
+         (size_t)kScaleSlots * kTileRows * sizeof(float);
+}
+
+template <int CL>
+__global__ void __launch_bounds__(kR8Threads, 1)
+    fwd_i8r_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sD = smem;
+  float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * kAtomBytes);
+  float* sScale = sPart + (size_t)2 * kR8Sets * 4 * 128;
+  __shared__ R8SmemHeader r8_hdr;
+  R8SmemHeader* hdr = &r8_hdr;
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int crank = (CL > 1) ? (int)cluster_ctarank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+  constexpr int kQCols = 32;
+
+  const long long n_workers = gridDim.x / CL;
+  const long long worker = blockIdx.x / CL;
+  const long long per = p.n_units / n_workers, rem = p.n_units % n_workers;
+  const long long u_begin = worker * per + min(worker, rem);
+  const long long u_end = u_begin + per + (worker < rem ? 1 : 0);
+  const int nmb_total = (p.l_q + kTileRows - 1) / kTileRows;
+  auto decode = [&](long long u, int& q, int& g, int& b) {
+    if (CL > 1) {
+      b = (int)(u % p.n_docs);
+      q = (int)(u / p.n_docs);
+      g = crank;
+    } else {
+      decode_unit(u, p, q, g, b);
+    }
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmD);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&hdr->full[s], 1);
+      mbar_init(&hdr->empty[s], CL);
+    }
+    for (int s = 0; s < kR8Sets; ++s) {
+      mbar_init(&hdr->tfull[s], 1);
+      mbar_init(&hdr->tempty[s], 4);
+    }
+    mbar_init(&hdr->qfull, kR8EpiWarps);
+    mbar_init(&hdr->qempty, 1);
+    for (int s = 0; s < kScaleSlots; ++s) {
+      mbar_init(&hdr->sfull[s], 1);
+      mbar_init(&hdr->sempty[s], kR8EpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  if (CL > 1) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = hdr->tmem_base;
+  constexpr uint32_t kIdesc = make_idesc(2, 1, 128, 128);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, sc_n = 0;
+      constexpr int kRowsPer = kTileRows / CL;
+      for (long long u = u_begin; u < u_end; ++u) {
+        int q, g, b;
+        decode(u, q, g, b);
+        const int vl = doc_valid_len(p, b);
+        const int ntiles = (vl + kTileRows - 1) / kTileRows;
+        for (int t = 0; t < ntiles; ++t) {
+          {
+            const int ss = (int)(sc_n % kScaleSlots);
+            mbar_wait_idle(&hdr->sempty[ss], ((sc_n / kScaleSlots) & 1u) ^ 1u);
+            const uint32_t bytes = (uint32_t)min(kTileRows, p.l_pad - t * kTileRows) * 4u;
+            mbar_arrive_expect_tx(&hdr->sfull[ss], bytes);
+            bulk_load_1d(&hdr->sfull[ss], sScale + ss * kTileRows,
+                         p.d_scale + (long long)b * p.l_pad + t * kTileRows, bytes, kEvictFirst);
+            ++sc_n;
+          }
+          mbar_wait_idle(&hdr->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)kAtomBytes);
+          const int row0 = b * p.l_pad + t * kTileRows + crank * kRowsPer;
+          uint8_t* dst = sD + (size_t)stage * kAtomBytes + crank * kRowsPer * 128;
+          if (CL > 1)
+            tma_load_2d_mc(&tmD, &hdr->full[stage], dst, 0, row0, kMask, kEvictFirst);
+          else
+            tma_load_2d(&tmD, &hdr->full[stage], dst, 0, row0, kEvictFirst);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (TS)
+    int stage = 0;
+    uint32_t phase = 0, qphase = 0;
+    uint32_t nblk = 0;  // accumulators produced so far: slot = nblk % 3
+    long long cur_key = -1;
+    const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
+    for (long long u = u_begin; u < u_end; ++u) {
+      int q, g, b;
+      decode(u, q, g, b);
+      const long long key = (long long)q * p.n_groups + g;
+      if (key != cur_key) {
+        if (cur_key >= 0) {
+          if (elect_one()) mma_commit(&hdr->qempty);
+          __syncwarp();
+        }
+        mbar_wait_idle(&hdr->qfull, qphase);
+        qphase ^= 1;
+        tc_fence_after();
+        cur_key = key;
+      }
+      const int qbv = min(p.qb, nmb_total - g * p.qb);
+      const int vl = doc_valid_len(p, b);
+      const int ntiles = (vl + kTileRows - 1) / kTileRows;
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait_idle(&hdr->full[stage], phase);
+        tc_fence_after();
+        const uint64_t bd0 = ddesc0 + (uint64_t)((stage * kAtomBytes) >> 4);
+        for (int mb = 0; mb < qbv; ++mb, ++nblk) {
+          const uint32_t slot = nblk % kR8Sets, use = nblk / kR8Sets;
+          mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
+            const uint32_t dcol = tmem_base + (uint32_t)(kR8AccCol0 + slot * 128);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_i8_ts(dcol, acol + k * 8, bd0 + (uint64_t)((k * 32) >> 4), kIdesc, k > 0 ? 1u : 0u);
+            mma_commit(&hdr->tfull[slot]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          if (CL > 1)
+            mma_commit_mc(&hdr->empty[stage], kMask);
+          else
+            mma_commit(&hdr->empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue sets
+    const int set = ((int)warp - 2) >> 2;
+    const int quad = (int)(warp & 3);
+    const int row_local = quad * 32 + (int)lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kR8AccCol0 + set * 128);
+    uint32_t nblk = 0, uses = 0, qeph = 0, sc_n = 0, ndoc = 0;
+    long long cur_key = -1;
+    for (long long u = u_begin; u < u_end; ++u) {
+      int q, g, b;
+      decode(u, q, g, b);
+      const int qbv = min(p.qb, nmb_total - g * p.qb);
+      const long long key = (long long)q * p.n_groups + g;
+      if (key != cur_key) {
+        if (cur_key >= 0) {
+          mbar_wait(&hdr->qempty, qeph);
+          qeph ^= 1;
+        }
+        // Q block mb is written by set mb % 3 (each warp its quadrant's 32 rows)
+        for (int mb = set; mb < qbv; mb += kR8Sets) {
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          const uint8_t* src = static_cast<const uint8_t*>(p.q_ptr) + ((long long)q * p.l_q + row) * p.dim;
+          uint32_t r[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+            if (row < p.l_q && c * 16 < p.dim) w = __ldg(reinterpret_cast<const uint4*>(src + c * 16));
+            r[4 * c] = w.x;
+            r[4 * c + 1] = w.y;
+            r[4 * c + 2] = w.z;
+            r[4 * c + 3] = w.w;
+          }
+          tmem_st32(tmem_base + lane_base + (uint32_t)(mb * kQCols), r);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hdr->qfull);
+        cur_key = key;
+      }
+      const int vl = doc_valid_len(p, b);
+      const int ntiles = (vl + kTileRows - 1) / kTileRows;
+      float part[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      float sq[4];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const int row = (g * p.qb + mb) * kTileRows + row_local;
+        sq[mb] = (mb < qbv && row < p.l_q) ? __ldg(p.q_scale + (long long)q * p.l_q + row) : 1.f;
+      }
+      for (int t = 0; t < ntiles; ++t) {
+        const int ss = (int)(sc_n % kScaleSlots);
+        mbar_wait(&hdr->sfull[ss], (sc_n / kScaleSlots) & 1u);
+        const float* sdt = sScale + ss * kTileRows;
+        const int base = t * kTileRows;
+        const bool full = base + kTileRows <= vl;
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) {
+          if (mb < qbv) {
+            if ((int)(nblk % kR8Sets) == set) {
+              mbar_wait(&hdr->tfull[set], uses & 1u);
+              ++uses;
+              tc_fence_after();
+              uint32_t ra[32], rb[32];
+              int cbd = 0;
+              tmem_ld32(taddr, ra);
+              tmem_ld32(taddr + 32, rb);
+              tmem_ld_wait();
+              if (full) {
+                ts_chunk_full<TcKind::I8, false>(ra, base, sq[mb], part[mb], cbd, nullptr, 0, sdt);
+                ts_chunk_full<TcKind::I8, false>(rb, base + 32, sq[mb], part[mb], cbd, nullptr, 0, sdt + 32);
+              } else {
+                ts_chunk<TcKind::I8, true>(ra, base, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt);
+                ts_chunk<TcKind::I8, true>(rb, base + 32, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 32);
+              }
+              tmem_ld32(taddr + 64, ra);
+              tmem_ld32(taddr + 96, rb);
+              tmem_ld_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&hdr->tempty[set]);
+              if (full) {
+                ts_chunk_full<TcKind::I8, false>(ra, base + 64, sq[mb], part[mb], cbd, nullptr, 0, sdt + 64);
+                ts_chunk_full<TcKind::I8, false>(rb, base + 96, sq[mb], part[mb], cbd, nullptr, 0, sdt + 96);
+              } else {
+                ts_chunk<TcKind::I8, true>(ra, base + 64, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 64);
+                ts_chunk<TcKind::I8, true>(rb, base + 96, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 96);
+              }
+            }
+            ++nblk;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hdr->sempty[ss]);
+        ++sc_n;
+      }
+      // ---- combine the three sets' partial maxima of this document (double-buffered by parity)
+      float* buf = sPart + (size_t)(ndoc & 1u) * kR8Sets * 4 * 128;
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) buf[(set * 4 + mb) * 128 + row_local] = part[mb];
+      named_bar_sync(1, 32 * kR8EpiWarps);
+      // set s writes out blocks mb with mb % 3 == s
+      const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
+      for (int mb = set; mb < qbv; mb += kR8Sets) {
+        const int row = (g * p.qb + mb) * kTileRows + row_local;
+        const float m = fmaxf(fmaxf(buf[(0 * 4 + mb) * 128 + row_local], buf[(1 * 4 + mb) * 128 + row_local]),
+                              buf[(2 * 4 + mb) * 128 + row_local]);
+        if (row < p.l_q) p.rowmax[obase + row] = m;
+      }
+      ++ndoc;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (CL > 1) cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace mxs
