@@ -60,6 +60,7 @@ from .varlen import PackedCorpus, fused_score_varlen, pack, score_varlen, unpack
 from .topk import TopKHeap, ranked, topk
 from .autograd import MaxSimFunction, MaxSimVarlenFunction, maxsim, maxsim_varlen
 from .training import contrastive_drift, softmax_ce
+from .reference import DenseSimTensor, dense_backward, dense_score, dense_score_batch, finite_diff_grad
 from .chamfer import PointSet, chamfer_backward, chamfer_forward, dense_chamfer_backward, dense_chamfer_forward
 from .streamio import (
     CorpusReader,
