@@ -83,6 +83,8 @@ def test_exact_fp32_c1_config_bitwise_and_ledger():
         (2, 520, 20, 400, 256, torch.bfloat16),
         (1, 130, 10, 129, 96, torch.bfloat16),
         (2, 1100, 6, 300, 128, torch.bfloat16),    # L_q > 1024: three Q row groups
+        (1, 640, 30, 512, 128, torch.bfloat16),    # two groups (4 + 1 blocks), 2-CTA cluster
+        (1, 384, 170, 256, 128, torch.bfloat16),   # one group of 3 blocks, more docs than SMs
     ],
 )
 def test_tensor_core_forward_vs_oracle(n_q, l_q, n_docs, l_pad, dim, dtype):
@@ -102,6 +104,9 @@ def test_tensor_core_forward_vs_oracle(n_q, l_q, n_docs, l_pad, dim, dtype):
     safe = top2_gap(Qo, Do, vl) > GAP
     assert np.array_equal(am.numpy()[safe], ref_a[safe])
     assert safe.mean() > 0.99
+    # rerank mode (no argmax): identical score bits
+    s2, a2, _ = mx.score_dense(Qr, Dr, cuda(vl), want_argmax=False)
+    assert a2 is None and np.array_equal(s2.cpu().numpy(), sc.numpy())
 
 
 def test_tensor_core_top20_agreement_planted():
