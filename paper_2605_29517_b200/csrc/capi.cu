@@ -576,6 +576,11 @@ int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, 
   const long long blocks = (rows * 32 + 255) / 256;
   if (dtype == MXS_F32)
     mxs::quantize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, rows, (int)dim, levels, q, scale);
+  else if (dtype == MXS_BF16 && dim == 128)
+    mxs::quantize128_kernel<__nv_bfloat16>
+        <<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, rows, levels, q, scale);
+  else if (dtype == MXS_F16 && dim == 128)
+    mxs::quantize128_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)x, rows, levels, q, scale);
   else if (dtype == MXS_BF16)
     mxs::quantize_kernel<__nv_bfloat16>
         <<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, rows, (int)dim, levels, q, scale);

@@ -7,6 +7,18 @@
 
 namespace mxs {
 
+// rint_half_even(fl32(x / s)) without an IEEE division per element: r = 1/s is within 1 ulp, so
+// y = x * r is within a few ulp of the correctly rounded quotient; the nearest integer can only
+// differ if y lies within a hair of a half-integer, and exactly those elements (rare) take the
+// exact __fdiv_rn path.  |x / s| <= levels + 1 <= 128, so 2^-12 is >> 4 ulp of y.
+MXS_DEV float quant_round(float x, float s, float r) {
+  const float y = __fmul_rn(x, r);
+  const float fy = floorf(y);
+  const float frac = y - fy;  // exact (Sterbenz-range subtraction)
+  if (fabsf(frac - 0.5f) < 0x1p-12f) return rintf(__fdiv_rn(x, s));
+  return rintf(y);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ x, long long rows, int dim, int levels,
                                                        int8_t* __restrict__ q, float* __restrict__ scale) {
@@ -21,13 +33,45 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ x, 
   float s = __fdiv_rn(mx, (float)levels);
   if (s == 0.f) s = 1e-12f;
   if (lane == 0) scale[warp] = s;
-  const float lv = (float)levels;
+  const float lv = (float)levels, r = __frcp_rn(s);
   int8_t* qr = q + warp * dim;
   for (int k = lane; k < dim; k += 32) {
-    float t = rintf(__fdiv_rn(to_f32(xr[k]), s));
+    float t = quant_round(to_f32(xr[k]), s, r);
     t = fminf(fmaxf(t, -lv), lv);
     qr[k] = (int8_t)(int)t;
   }
+}
+
+// Vectorised variant for bf16 / f16 rows with dim == 128: a warp owns a row, a lane 4 elements
+// (one 8-byte load, one 4-byte int8 store); the row stays in registers for both passes.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize128_kernel(const T* __restrict__ x, long long rows, int levels,
+                                                          int8_t* __restrict__ q, float* __restrict__ scale) {
+  static_assert(sizeof(T) == 2, "16-bit rows");
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + warp * 128) + lane);
+  float v[4];
+  {
+    const T* h = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = to_f32(h[j]);
+  }
+  float mx = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = __fdiv_rn(mx, (float)levels);
+  if (s == 0.f) s = 1e-12f;
+  if (lane == 0) scale[warp] = s;
+  const float r = __frcp_rn(s), lv = (float)levels;
+  uint32_t packed = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float t = fminf(fmaxf(quant_round(v[j], s, r), -lv), lv);
+    packed |= ((uint32_t)(uint8_t)(int8_t)(int)t) << (8 * j);
+  }
+  reinterpret_cast<uint32_t*>(q + warp * 128)[lane] = packed;
 }
 
 }  // namespace mxs

@@ -174,6 +174,25 @@ def test_quantize_bitwise_against_golden():
     assert np.all(z.scale.cpu().numpy() == np.float32(1e-12))
 
 
+@pytest.mark.parametrize("dim,dtype", [(128, torch.bfloat16), (128, torch.float16), (96, torch.bfloat16),
+                                       (128, torch.float32)])
+def test_quantize_half_way_quotients(dim, dtype):
+    """Reciprocal fast path + exact-division fallback: quotients exactly on / next to k + 0.5."""
+    rng = np.random.default_rng(dim)
+    x = np.zeros((64, dim), np.float32)
+    x[:, 0] = 127.0                                          # scale 1 (maxabs / 127)
+    halves = rng.integers(-126, 126, (64, dim - 1)) + 0.5   # exact ties -> even
+    x[:, 1:] = halves
+    x[1::3, 1:] = np.nextafter(halves[1::3], np.inf)          # just above a tie
+    x[2::3, 1:] = np.nextafter(halves[2::3], -np.inf)         # just below
+    x[40:] *= rng.uniform(0.001, 30, (24, 1)).astype(np.float32)  # other scales
+    xt = cuda(x, dtype)
+    xr = xt.float().cpu().numpy()                             # the values the device sees
+    q, sc = orc.quantize_per_token(xr)
+    qm, sm = mx.quant.quantize_tensor(xt)
+    assert np.array_equal(qm.cpu().numpy(), q) and np.array_equal(sm.cpu().numpy(), sc)
+
+
 def test_quantize_random_bitwise_vs_oracle():
     rng = np.random.default_rng(8)
     x = (rng.standard_normal((777, 130)) * rng.uniform(0.01, 10, (777, 1))).astype(np.float32)
