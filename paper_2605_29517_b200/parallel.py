@@ -112,3 +112,34 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     if work is not None:
         work.wait()
     return loss, scores, dQ, dD.reshape(b_local, l_pad, dim)
+
+
+class InBatchStepGraph:
+    """`inbatch_step` captured once into a CUDA graph and replayed (single process).
+
+    A training loop updates Q and D in place between steps; the graph reads those same buffers,
+    so every replay is one launch of the whole step (forward kernel, f64 score fold, loss,
+    device CSR, the two gather kernels) with no per-kernel host launch cost.  Outputs are the
+    graph's static tensors (copy them if they must survive the next replay).
+    """
+
+    def __init__(self, Q: torch.Tensor, D: torch.Tensor, warmup: int = 2):
+        import torch.distributed as dist
+
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            raise ValueError("InBatchStepGraph is the single-GPU step; use inbatch_step across ranks")
+        self.Q, self.D = Q, D
+        side = torch.cuda.Stream(device=Q.device)
+        side.wait_stream(torch.cuda.current_stream(Q.device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):  # allocator warm-up outside the capture
+                inbatch_step(Q, D, 0)
+        torch.cuda.current_stream(Q.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = inbatch_step(Q, D, 0)
+
+    def __call__(self):
+        """Replay: returns (loss, scores, dQ, dD) -- the graph's static output tensors."""
+        self.graph.replay()
+        return self.out

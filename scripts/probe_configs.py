@@ -34,7 +34,10 @@ t_csr = timeit(lambda: csr_tensors(am, off, lens, 65536, 1024))
 t_dd = timeit(lambda: _grad_docs(Q, am, gq, off, lens, 65536, 1024, 128))
 t_dq = timeit(lambda: _grad_query(D.reshape(-1, 128), off, am, gq, 128))
 t_step = timeit(lambda: inbatch_step(Q, D, 0))
-print(f"C3 fwd {t_fwd:.3f} ms ({1.0995e12 / t_fwd / 1e9:.0f} TF/s) | csr {t_csr:.3f} | csr+dD {t_dd:.3f} | dQ {t_dq:.3f} | full step {t_step:.3f} ms")
+from paper_2605_29517_b200.parallel import InBatchStepGraph
+gstep = InBatchStepGraph(Q, D)
+t_gstep = timeit(gstep)
+print(f"C3 fwd {t_fwd:.3f} ms ({1.0995e12 / t_fwd / 1e9:.0f} TF/s) | csr {t_csr:.3f} | csr+dD {t_dd:.3f} | dQ {t_dq:.3f} | full step {t_step:.3f} ms | graph step {t_gstep:.3f} ms")
 
 # C4: INT8 10K docs
 nb = 10000

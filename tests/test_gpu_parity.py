@@ -357,6 +357,21 @@ def test_inbatch_training_step_c3_shape_bf16():
     assert rel_err(dD.cpu().numpy(), dd_ref) < REL
 
 
+def test_inbatch_step_graph_replay_matches_eager():
+    from paper_2605_29517_b200.parallel import InBatchStepGraph, inbatch_step
+
+    rng = np.random.default_rng(12)
+    Q = cuda(orc.make_queries(8, 256, 128, seed=1), torch.bfloat16)
+    D = cuda(orc.make_queries(8, 200, 128, seed=2), torch.bfloat16)
+    g = InBatchStepGraph(Q, D)
+    for _ in range(2):
+        loss, sc, dq, dd = g()
+        el, es, edq, edd = inbatch_step(Q, D, 0)
+        assert float(loss) == float(el) and torch.equal(sc, es)
+        assert torch.equal(dq, edq) and torch.equal(dd, edd)
+        D.add_(torch.from_numpy(rng.standard_normal(D.shape) * 0.01).cuda().bfloat16())  # in-place update
+
+
 def test_autograd_matches_oracle_and_finite_differences():
     g = golden("inbatch")
     Q = cuda(g["Q"]).requires_grad_(True)
