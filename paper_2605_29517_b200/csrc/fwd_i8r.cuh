@@ -250,42 +250,47 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         const float* sdt = sScale + ss * kTileRows;
         const int base = t * kTileRows;
         const bool full = base + kTileRows <= vl;
-#pragma unroll
-        for (int mb = 0; mb < 4; ++mb) {
-          if (mb < qbv) {
-            if ((int)(nblk % kR8Sets) == set) {
-              mbar_wait(&hdr->tfull[set], uses & 1u);
-              ++uses;
-              tc_fence_after();
-              uint32_t ra[32], rb[32];
-              int cbd = 0;
-              tmem_ld32(taddr, ra);
-              tmem_ld32(taddr + 32, rb);
-              tmem_ld_wait();
-              if (full) {
-                ts_chunk_full<TcKind::I8, false>(ra, base, sq[mb], part[mb], cbd, nullptr, 0, sdt);
-                ts_chunk_full<TcKind::I8, false>(rb, base + 32, sq[mb], part[mb], cbd, nullptr, 0, sdt + 32);
-              } else {
-                ts_chunk<TcKind::I8, true>(ra, base, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt);
-                ts_chunk<TcKind::I8, true>(rb, base + 32, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 32);
-              }
-              tmem_ld32(taddr + 64, ra);
-              tmem_ld32(taddr + 96, rb);
-              tmem_ld_wait();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&hdr->tempty[set]);
-              if (full) {
-                ts_chunk_full<TcKind::I8, false>(ra, base + 64, sq[mb], part[mb], cbd, nullptr, 0, sdt + 64);
-                ts_chunk_full<TcKind::I8, false>(rb, base + 96, sq[mb], part[mb], cbd, nullptr, 0, sdt + 96);
-              } else {
-                ts_chunk<TcKind::I8, true>(ra, base + 64, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 64);
-                ts_chunk<TcKind::I8, true>(rb, base + 96, vl, p, b, sq[mb], part[mb], cbd, nullptr, 0, sdt + 96);
-              }
-            }
-            ++nblk;
+        // this set's blocks of the tile (one or two of the four); a rolled loop keeps the code
+        // small enough for the instruction cache -- the per-block state is selected by value
+        const int first = (int)((kR8Sets + set - (int)(nblk % kR8Sets)) % kR8Sets);
+#pragma unroll 1
+        for (int mb = first; mb < qbv; mb += kR8Sets) {
+          float pm = mb == 0 ? part[0] : mb == 1 ? part[1] : mb == 2 ? part[2] : part[3];
+          const float sqm = mb == 0 ? sq[0] : mb == 1 ? sq[1] : mb == 2 ? sq[2] : sq[3];
+          mbar_wait(&hdr->tfull[set], uses & 1u);
+          ++uses;
+          tc_fence_after();
+          uint32_t ra[32], rb[32];
+          int cbd = 0;
+          tmem_ld32(taddr, ra);
+          tmem_ld32(taddr + 32, rb);
+          tmem_ld_wait();
+          if (full) {
+            ts_chunk_full<TcKind::I8, false>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk_full<TcKind::I8, false>(rb, base + 32, sqm, pm, cbd, nullptr, 0, sdt + 32);
+          } else {
+            ts_chunk<TcKind::I8, true>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk<TcKind::I8, true>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 32);
           }
+          tmem_ld32(taddr + 64, ra);
+          tmem_ld32(taddr + 96, rb);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hdr->tempty[set]);
+          if (full) {
+            ts_chunk_full<TcKind::I8, false>(ra, base + 64, sqm, pm, cbd, nullptr, 0, sdt + 64);
+            ts_chunk_full<TcKind::I8, false>(rb, base + 96, sqm, pm, cbd, nullptr, 0, sdt + 96);
+          } else {
+            ts_chunk<TcKind::I8, true>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 64);
+            ts_chunk<TcKind::I8, true>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 96);
+          }
+          part[0] = mb == 0 ? pm : part[0];
+          part[1] = mb == 1 ? pm : part[1];
+          part[2] = mb == 2 ? pm : part[2];
+          part[3] = mb == 3 ? pm : part[3];
         }
+        nblk += (uint32_t)qbv;
         __syncwarp();
         if (lane == 0) mbar_arrive(&hdr->sempty[ss]);
         ++sc_n;
