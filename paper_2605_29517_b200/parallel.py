@@ -31,7 +31,7 @@ def shard_bounds(n_docs: int, world: int, rank: int, weights=None):
     return min(lo, n_docs), min(hi, n_docs)
 
 
-def sharded_topk(local_scores: torch.Tensor, k: int, doc_offset: int, group=None):
+def sharded_topk(local_scores: torch.Tensor, k: int, doc_offset: int, group=None, select=None):
     """Global top-K of a doc-sharded score vector: device top-K per rank, then one all_gather."""
     kk = min(k, local_scores.numel())
     ts, ti = topk(local_scores, kk, id_offset=doc_offset)
@@ -39,7 +39,7 @@ def sharded_topk(local_scores: torch.Tensor, k: int, doc_offset: int, group=None
         pad = k - kk
         ts = torch.cat([ts, torch.full((pad,), float("-inf"), dtype=ts.dtype, device=ts.device)])
         ti = torch.cat([ti, torch.full((pad,), -1, dtype=ti.dtype, device=ti.device)])
-    return merge_topk_across_ranks(ts, ti, k, group=group)
+    return merge_topk_across_ranks(ts, ti, k, group=group, select=select)
 
 
 def softmax_ce(scores: torch.Tensor):

@@ -3,8 +3,8 @@
 * `TopKHeap` mirrors maxsim/streamio.py:230-262 on the host (small, streaming merges).
 * `topk` runs the device selection kernel (K9) over an f64 score vector.
 * `merge_topk_across_ranks` all-gathers each rank's (score, global id) candidates over
-  torch.distributed (NCCL on the GPU box, gloo in CPU tests) and re-selects with the same
-  ordering, so a sharded corpus ranks exactly like the unsharded one.
+  torch.distributed (NCCL) and re-selects them on the device with the same ordering, so a
+  sharded corpus ranks exactly like the unsharded one.
 """
 
 from __future__ import annotations
@@ -80,31 +80,24 @@ def ranked(scores, k: int | None = None):
 
 
 def select_candidates(scores: torch.Tensor, ids: torch.Tensor, k: int, stream=None):
-    """Top-K among (score, id) candidates with explicit ids (ids < 0 are empty slots).
-
-    On CUDA tensors this is one single-block selection kernel; CPU tensors (gloo tests of the
-    host-side merge logic) use the identical ordering in Python.
-    """
-    if scores.is_cuda:
-        s = scores.reshape(-1).to(torch.float64).contiguous()
-        i = ids.reshape(-1).to(torch.int64).contiguous()
-        top_s = torch.empty(k, dtype=torch.float64, device=s.device)
-        top_i = torch.empty(k, dtype=torch.int64, device=s.device)
-        _lib.call("mxs_topk_candidates", _dev.ptr(s), _dev.ptr(i), s.numel(), k, _dev.ptr(top_s), _dev.ptr(top_i),
-                  _dev.stream_handle(stream))
-        return top_s, top_i
-    s = scores.reshape(-1).to(torch.float64).cpu()
-    i = ids.reshape(-1).to(torch.int64).cpu()
-    keep = i >= 0
-    s, i = s[keep], i[keep]
-    order = sorted(range(s.numel()), key=lambda j: (-float(s[j]), int(i[j])))[:k]
-    return s[order], i[order]
+    """Top-K among (score, id) candidates with explicit ids (ids < 0 are empty slots): one
+    single-block selection kernel on the device (no host path)."""
+    s = scores.reshape(-1).to(torch.float64).contiguous()
+    i = ids.reshape(-1).to(torch.int64).contiguous()
+    _dev.require_cuda(s, i)
+    top_s = torch.empty(k, dtype=torch.float64, device=s.device)
+    top_i = torch.empty(k, dtype=torch.int64, device=s.device)
+    _lib.call("mxs_topk_candidates", _dev.ptr(s), _dev.ptr(i), s.numel(), k, _dev.ptr(top_s), _dev.ptr(top_i),
+              _dev.stream_handle(stream))
+    return top_s, top_i
 
 
-def merge_topk_across_ranks(top_s: torch.Tensor, top_id: torch.Tensor, k: int, group=None):
+def merge_topk_across_ranks(top_s: torch.Tensor, top_id: torch.Tensor, k: int, group=None, select=None):
     """All-gather every rank's K candidates and re-select the global top-K (same tie rule).
 
-    The payload is k * 16 bytes per rank; with NCCL it is one all_gather on the device.
+    The payload is k * 16 bytes per rank; with NCCL it is one all_gather of device tensors
+    straight into the device selection kernel.  `select` replaces that kernel (the CPU gloo tests
+    pass an oracle-backed twin; the product path always uses `select_candidates`).
     """
     import torch.distributed as dist
 
@@ -113,4 +106,4 @@ def merge_topk_across_ranks(top_s: torch.Tensor, top_id: torch.Tensor, k: int, g
     gi = [torch.empty_like(top_id) for _ in range(world)]
     dist.all_gather(gs, top_s.contiguous(), group=group)
     dist.all_gather(gi, top_id.contiguous(), group=group)
-    return select_candidates(torch.cat(gs), torch.cat(gi), k)
+    return (select or select_candidates)(torch.cat(gs), torch.cat(gi), k)

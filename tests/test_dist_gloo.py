@@ -20,6 +20,16 @@ def _free_port():
     return port
 
 
+def cpu_select(scores, ids, k):
+    """CPU twin of topk.select_candidates (the reference order: score desc, id asc), for gloo."""
+    s = scores.reshape(-1).to(torch.float64)
+    i = ids.reshape(-1).to(torch.int64)
+    keep = i >= 0
+    s, i = s[keep], i[keep]
+    order = sorted(range(s.numel()), key=lambda j: (-float(s[j]), int(i[j])))[:k]
+    return s[order], i[order]
+
+
 class OracleKernels:
     """CPU twin of parallel.DeviceKernels (f64 oracle arithmetic), for the collective logic only."""
 
@@ -47,14 +57,14 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2605_29517_b200.parallel import inbatch_step, shard_bounds
-        from paper_2605_29517_b200.topk import merge_topk_across_ranks, select_candidates
+        from paper_2605_29517_b200.topk import merge_topk_across_ranks
 
         # ---- sharded rerank: per-rank top-K + all_gather merge == global ranking
         rng = np.random.default_rng(5)
         scores = np.round(rng.standard_normal(103), 1)  # many exact ties
         lo, hi = shard_bounds(103, world, rank)
-        ls, li = select_candidates(torch.tensor(scores[lo:hi]), torch.arange(lo, hi), 7)
-        ts, ti = merge_topk_across_ranks(ls, li, 7)
+        ls, li = cpu_select(torch.tensor(scores[lo:hi]), torch.arange(lo, hi), 7)
+        ts, ti = merge_topk_across_ranks(ls, li, 7, select=cpu_select)
         os_, oi = orc.topk(scores, 7)
         ok_topk = ti.tolist() == oi.tolist() and ts.tolist() == os_.tolist()
 
@@ -84,8 +94,8 @@ def _worker(rank, world, port, q):
         lo, hi = shard_bounds(61, world, rank, weights=lens)
         loc_cu = cu[lo:hi + 1] - cu[lo]
         loc_s, _ = orc.fused_score_varlen(qv[None], toks[cu[lo]:cu[hi]], loc_cu)
-        ls, li = select_candidates(torch.from_numpy(loc_s[0]), torch.arange(lo, hi), 9)
-        ts, ti = merge_topk_across_ranks(ls, li, 9)
+        ls, li = cpu_select(torch.from_numpy(loc_s[0]), torch.arange(lo, hi), 9)
+        ts, ti = merge_topk_across_ranks(ls, li, 9, select=cpu_select)
         g_s, _ = orc.fused_score_varlen(qv[None], toks, cu)
         os_, oi = orc.topk(g_s[0], 9)
         tok_share = (cu[hi] - cu[lo]) / cu[-1]
