@@ -4,7 +4,8 @@
 //   A = the n_cols = n_q * l_q (<= 128) query rows, replicated C = 128 / round_up(n_cols) times
 //       (C = 4 for ColBERT's L_q = 32) so that every TMEM lane quadrant holds real rows;
 //   B = a tile of 128 consecutive packed tokens (TMA from the [total_tokens, dim] buffer);
-//   D = [128 lanes x 128 tokens] fp32 in one of two TMEM slots.
+//   D = [128 lanes x 128 tokens] fp32 in one of four TMEM slots (slot = tile % 4, so each scan
+//       set double-buffers and the MMA runs up to two tiles ahead of the drain).
 // Copy k of the rows scans token range k of the tile (128 / C tokens): each epilogue thread owns
 // one query row and folds the range's tokens IN ORDER straight out of its registers
 // (tcgen05.ld), keeping (max, first argmax) per document piece -- strict >, so the earliest
@@ -38,6 +39,7 @@ struct VarlenRowsParams {
 constexpr int kVrTile = 128;       // tokens per tile (MMA N)
 constexpr int kVrThreads = 32 * 15;  // warp 0 TMA, 1 MMA + TMEM, 2..9 scan, 10 boundaries, 11..14 merge
 constexpr int kVrSlotCols = 128;
+constexpr int kVrSlots = 4;
 constexpr int kVrInfoSlots = 16;
 constexpr int kVrPieceBufs = 4;
 
@@ -60,8 +62,8 @@ struct VrShared {
 struct VrSmemHeader {
   uint64_t full[8];
   uint64_t empty[8];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
+  uint64_t tfull[kVrSlots];
+  uint64_t tempty[kVrSlots];
   uint64_t qfull;
   uint64_t ifull[kVrInfoSlots];
   uint64_t iempty[kVrInfoSlots];
@@ -160,12 +162,12 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
     const long long dstart_first = sh->info[islot].dstart_first;
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->iempty[islot]);
-    const uint32_t slot = (uint32_t)set;
+    const uint32_t slot = (uint32_t)t & (kVrSlots - 1);  // = set or set + 2
     const int pb = (t >> 1) % kVrPieceBufs;
     const int x1 = min(x0 + L, ntok);
     float m = -INFINITY, hm = -INFINITY;
     int a = 0, ha = 0;
-    mbar_wait(&hdr->tfull[slot], ((uint32_t)t >> 1) & 1u);
+    mbar_wait(&hdr->tfull[slot], ((uint32_t)t >> 2) & 1u);
     tc_fence_after();
     if (x0 < ntok) {
       long long doc = d_first + vr_popc_range(w, 1, x0 + 1);
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       mbar_init(&hdr->full[s], 1);
       mbar_init(&hdr->empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kVrSlots; ++s) {
       mbar_init(&hdr->tfull[s], 1);
       mbar_init(&hdr->tempty[s], (uint32_t)n_active);
     }
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&hdr->tmem_base, 256);
+  if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -440,9 +442,9 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < n_tiles; ++t) {
-        const int slot = t & 1;
+        const int slot = t & (kVrSlots - 1);
         mbar_wait_idle(&hdr->full[stage], phase);
-        mbar_wait_idle(&hdr->tempty[slot], (((uint32_t)t >> 1) & 1u) ^ 1u);
+        mbar_wait_idle(&hdr->tempty[slot], (((uint32_t)t >> 2) & 1u) ^ 1u);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t bd0 = tdesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       vr_merge<1>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
   } else {
     // ------------------------------------------------------------------ scan
-    const int set = ((int)warp - 2) >> 2;  // tiles t with t % 2 == set, TMEM slot `set`
+    const int set = ((int)warp - 2) >> 2;  // tiles t with t % 2 == set, TMEM slots set and set + 2
     const int quad = (int)(warp & 3);      // TMEM lane quadrant (hardware rule: warp id % 4)
     if (C == 4)
       vr_scan<KIND, KA, 4>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(kVrThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 256);
+    tmem_dealloc(tmem_base, 512);
   }
 }
 
