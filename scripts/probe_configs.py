@@ -21,6 +21,14 @@ def unit(*shape):
     x = torch.randn(*shape, device="cuda", generator=g)
     return (x / x.norm(dim=-1, keepdim=True)).bfloat16()
 
+# C1: ColBERT rerank, 1 query L_q=32 vs 1000 docs L_d=180, d=128, FP32 -> the bit-exact fp32 kernel
+q1 = torch.randn(1, 32, 128, device="cuda", generator=g)
+q1 = q1 / q1.norm(dim=-1, keepdim=True)
+d1 = torch.randn(1000, 180, 128, device="cuda", generator=g)
+d1 = d1 / d1.norm(dim=-1, keepdim=True)
+t_c1 = timeit(lambda: mx.score_dense(q1, d1))
+print(f"C1 fp32 exact {t_c1:.3f} ms ({1000 / t_c1 * 1e3 / 1e6:.2f} M docs/s, {1.47456e9 / t_c1 / 1e9:.2f} TFLOP/s fp32)")
+
 # C3: in-batch 64 x 64 ColPali shape
 Q = unit(64, 1024, 128); D = unit(64, 1024, 128)
 t_fwd = timeit(lambda: mx.score_dense(Q, D))
