@@ -239,7 +239,11 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   const int nmb = (int)((l_q + 127) / 128);
   const int qb = std::min(qb_max, nmb);
   const int n_groups = (nmb + qb - 1) / qb;
-  const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
+  int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
+  {
+    const char* f = getenv("MXS_FWD_CL");  // profiling knob: force the cluster size (1 = no multicast)
+    if (f && atoi(f) == 1) cl = 1;
+  }
   const size_t max_smem = 232448 - sizeof(mxs::TsSmemHeader);  // static header comes out of the same 227 KB
   const bool scale_ring = (KIND == mxs::TcKind::I8) && (l_pad % 4 == 0);
   const size_t fixed = mxs::fwd_ts_smem_bytes(0, qb, 0, scale_ring);
