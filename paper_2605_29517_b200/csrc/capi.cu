@@ -52,6 +52,31 @@ int sm_count() {
   return n;
 }
 
+// Persistent cluster grids: as many clusters of `cl` CTAs as the device can keep resident at
+// once (clusters of 4 do not tile every GPC, so nsm / 4 may over-subscribe and leave a tail
+// wave); falls back to nsm / cl if the occupancy query fails.
+template <typename KernT>
+long long resident_clusters(KernT kern, int cl, int threads, size_t smem, int nsm) {
+  if (cl <= 1) return nsm;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((nsm / cl) * cl));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return nsm / cl;
+  }
+  return std::min<long long>(n, nsm / cl);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -159,23 +184,28 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   return check_launch("fwd_tc_kernel");
 }
 
-// INT8 rerank path (argmax not requested, d <= 128): three epilogue warp sets (fwd_i8r.cuh).
-// Returns MXS_UNSUPPORTED (without launching) otherwise.
-int launch_fwd_i8r(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad,
-                   int64_t dim, const int32_t* valid_lens, const float* q_scale, const float* d_scale, float* rowmax,
-                   cudaStream_t st) {
-  if (dim % 16 != 0 || dim > 128 || l_pad % 4 != 0) return MXS_UNSUPPORTED;
+// Rerank path (argmax not requested): three accumulator slots / three epilogue warp sets
+// (fwd_i8r.cuh).  INT8 with d <= 128 (4 resident Q blocks), bf16 / fp16 with d <= 128 (2 resident
+// Q blocks, 4-CTA clusters at L_q = 1024).  Returns MXS_UNSUPPORTED (without launching) otherwise.
+template <mxs::TcKind KIND>
+int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad, int64_t dim,
+                  const int32_t* valid_lens, const float* q_scale, const float* d_scale, float* rowmax,
+                  cudaStream_t st) {
+  constexpr bool kI8 = KIND == mxs::TcKind::I8;
+  const int eb = kI8 ? 1 : 2;
+  if (dim % 16 != 0 || dim > 128 || (kI8 && l_pad % 4 != 0)) return MXS_UNSUPPORTED;
   {
-    const char* impl = getenv("MXS_I8_IMPL");
+    const char* impl = getenv(kI8 ? "MXS_I8_IMPL" : "MXS_RERANK_IMPL");
     if (impl && strcmp(impl, "ts") == 0) return MXS_UNSUPPORTED;
   }
+  constexpr int ka = kI8 ? 1 : 2;
   const int nmb = (int)((l_q + 127) / 128);
-  const int qb = std::min(mxs::kMaxQb, nmb);
+  const int qb = std::min(kI8 ? 4 : 2, nmb);
   const int n_groups = (nmb + qb - 1) / qb;
   const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
   const size_t max_smem = 232448 - sizeof(mxs::R8SmemHeader);
-  const size_t fixed = mxs::fwd_i8r_smem_bytes(0);
-  int stages = (int)((max_smem - fixed) / (size_t)mxs::kAtomBytes);
+  const size_t fixed = mxs::fwd_i8r_smem_bytes(ka, 0);
+  int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
   mxs::FwdTcParams p = {};
@@ -184,7 +214,7 @@ int launch_fwd_i8r(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64
   p.n_docs = (int)n_docs;
   p.l_pad = (int)l_pad;
   p.dim = (int)dim;
-  p.ka = 1;
+  p.ka = ka;
   p.qb = qb;
   p.n_groups = n_groups;
   p.stages = stages;
@@ -195,17 +225,22 @@ int launch_fwd_i8r(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64
   p.rowmax = rowmax;
   p.argmax = nullptr;
   p.q_ptr = Q;
+  const CUtensorMapDataType dt = kI8                         ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : KIND == mxs::TcKind::BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap td;
   int s;
-  if ((s = make_tmap_2d(&td, D, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
-  const size_t smem = mxs::fwd_i8r_smem_bytes(stages);
+  if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
+  const size_t smem = mxs::fwd_i8r_smem_bytes(ka, stages);
   using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
-  KernT kern = cl == 4 ? mxs::fwd_i8r_kernel<4> : (cl == 2 ? mxs::fwd_i8r_kernel<2> : mxs::fwd_i8r_kernel<1>);
+  KernT kern = cl == 4   ? mxs::fwd_i8r_kernel<KIND, ka, 4>
+               : cl == 2 ? mxs::fwd_i8r_kernel<KIND, ka, 2>
+                         : mxs::fwd_i8r_kernel<KIND, ka, 1>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
   const int nsm = sm_count();
   if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
-  long long workers = nsm / cl;
+  long long workers = resident_clusters(kern, cl, mxs::kR8Threads, smem, nsm);
   if (p.n_units < workers) workers = p.n_units;
   if (workers <= 0) return MXS_OK;
   cudaLaunchConfig_t cfg = {};
@@ -290,7 +325,7 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
     return fail(MXS_CUDA_ERROR, "cudaFuncSetAttribute(smem=%zu) failed", smem);
   const int nsm = sm_count();
   if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
-  long long workers = nsm / cl;
+  long long workers = resident_clusters(kern, cl, mxs::kTsThreads, smem, nsm);
   if (p.n_units < workers) workers = p.n_units;
   if (workers <= 0) return MXS_OK;
   cudaLaunchConfig_t cfg = {};
@@ -368,6 +403,11 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
     if ((s = check_launch("varlen_rows_kernel")) != MXS_OK) return s;
   }
   return MXS_OK;
+}
+
+bool rerank_r3_opt_in() {
+  const char* impl = getenv("MXS_RERANK_IMPL");
+  return impl && strcmp(impl, "r3") == 0;
 }
 
 bool use_ts_path() {
@@ -528,16 +568,28 @@ int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     else
       return fail(MXS_UNSUPPORTED, "mxs_fused_score_batch: dtype %d not a float type", dtype);
   } else if (dtype == MXS_BF16) {
-    s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
-                                                         nullptr, rowmax, argmax, st)
-                      : MXS_UNSUPPORTED;
+    // bf16 rerank: the three-slot kernel (2 resident Q blocks) measured 1.83 ms vs 1.76 ms for
+    // fwd_ts at the C2 shape, so it is opt-in (MXS_RERANK_IMPL=r3)
+    s = (argmax || !rerank_r3_opt_in())
+            ? MXS_UNSUPPORTED
+            : launch_fwd_r3<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr,
+                                               rowmax, st);
+    if (s == MXS_UNSUPPORTED)
+      s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
+                                                           nullptr, rowmax, argmax, st)
+                        : MXS_UNSUPPORTED;
     if (s == MXS_UNSUPPORTED)
       s = launch_fwd_tc<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
                                            argmax, st);
   } else if (dtype == MXS_F16) {
-    s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
-                                                        nullptr, rowmax, argmax, st)
-                      : MXS_UNSUPPORTED;
+    s = (argmax || !rerank_r3_opt_in())
+            ? MXS_UNSUPPORTED
+            : launch_fwd_r3<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr,
+                                              rowmax, st);
+    if (s == MXS_UNSUPPORTED)
+      s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr,
+                                                          nullptr, rowmax, argmax, st)
+                        : MXS_UNSUPPORTED;
     if (s == MXS_UNSUPPORTED)
       s = launch_fwd_tc<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
                                           argmax, st);
@@ -557,7 +609,8 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
   if (dim > 133000) return fail(MXS_SHAPE_MISMATCH, "dim %lld exceeds 133000 (int32 accumulation bound)", (long long)dim);
   cudaStream_t st = (cudaStream_t)stream;
   int s = argmax ? MXS_UNSUPPORTED
-                 : launch_fwd_i8r(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale, rowmax, st);
+                 : launch_fwd_r3<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale,
+                                                  rowmax, st);
   if (s == MXS_UNSUPPORTED)
     s = use_ts_path() ? launch_fwd_ts<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale,
                                                          d_scale, rowmax, argmax, st)

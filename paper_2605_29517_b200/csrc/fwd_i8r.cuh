@@ -1,19 +1,23 @@
-// INT8 x INT8 forward, RERANK mode (argmax not requested): scores only -- maxsim/quant.py:128-182
-// with the per-token maxima reduced to the f64 score, no index tracking.
+// Forward in RERANK mode (argmax not requested): scores only -- maxsim/forward.py:108-155 and
+// maxsim/quant.py:128-182 with the per-token maxima reduced to the f64 score, no index tracking.
 //
-// The INT8 epilogue is issue-bound (the reference's dequantise-before-max, S7, costs ~3 issued
-// instructions per similarity), so this variant puts THREE epilogue warp sets on the SM instead
-// of two.  Without argmax tracking the running row maximum is order-free (max is exact and
-// commutative), which is what makes the split legal:
+// Three accumulator slots instead of two.  With two, the MMA of Q block n + 2 waits until the
+// accumulator of block n has been committed, drained and released -- a handshake that outlasts
+// the 512-cycle MMA of block n + 1 (measured: the bf16 forward ran at ~70 % of the raw TS-MMA rate
+// with the epilogue disabled).  With three, two blocks of work are always queued.  TMEM holds
+// 128 columns of resident Q (4 INT8 blocks, or 2 bf16/fp16 blocks -- bf16 then uses 4-CTA
+// clusters) plus 3 x 128 accumulator columns.  THREE epilogue warp sets also give the
+// issue-bound INT8 epilogue (the reference's dequantise-before-max, S7, ~3 issued instructions
+// per similarity) more warps.  Without argmax tracking the running row maximum is order-free
+// (max is exact and commutative), which is what makes the split legal:
 //   * the MMA issuer numbers every (tile, Q block) accumulator it produces, n = 0, 1, 2, ...;
 //     accumulator n lands in TMEM slot n % 3 and is drained by epilogue set n % 3, so each set
 //     consumes its own slot in order (no mbarrier phase aliasing);
 //   * each set keeps, per Q block, a partial maximum over the tiles it happened to drain; at the
 //     end of a document the three partials of every row are max-combined through shared memory
 //     (double-buffered by document parity) and written once.
-// TMEM: 4 Q blocks x 32 columns (d <= 128) + 3 slots x 128 columns = 512.  Everything else
-// (TS MMA with Q resident in TMEM, cluster multicast of document tiles, TMA-staged scales,
-// magic-number s32 -> f32) is fwd_ts.cuh's.
+// Everything else (TS MMA with Q resident in TMEM, cluster multicast of document tiles,
+// TMA-staged INT8 scales, magic-number s32 -> f32) is fwd_ts.cuh's.
 #pragma once
 #include "fwd_ts.cuh"
 
@@ -39,18 +43,19 @@ struct R8SmemHeader {
 
 // dynamic smem: document tiles + per-document partial maxima [2 docs][3 sets][4 blocks][128 rows]
 // + the scale ring
-__host__ __device__ inline size_t fwd_i8r_smem_bytes(int stages) {
-  return 1024 + (size_t)stages * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
+__host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages) {
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
          (size_t)kScaleSlots * kTileRows * sizeof(float);
 }
 
-template <int CL>
+template <TcKind KIND, int KA, int CL>
 __global__ void __launch_bounds__(kR8Threads, 1)
     fwd_i8r_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
+  static_assert(KA * 32 * (KIND == TcKind::I8 ? 4 : 2) <= 128, "resident Q must fit 128 TMEM columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sD = smem;
-  float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * kAtomBytes);
+  float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
   float* sScale = sPart + (size_t)2 * kR8Sets * 4 * 128;
   __shared__ R8SmemHeader r8_hdr;
   R8SmemHeader* hdr = &r8_hdr;
@@ -59,7 +64,9 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   const uint32_t lane = lane_id();
   const int crank = (CL > 1) ? (int)cluster_ctarank() : 0;
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
-  constexpr int kQCols = 32;
+  constexpr int kQCols = KA * 32;
+  constexpr bool kI8 = KIND == TcKind::I8;
+  constexpr int kElemsPerAtom = kI8 ? 128 : 64;
 
   const long long n_workers = gridDim.x / CL;
   const long long worker = blockIdx.x / CL;
@@ -101,7 +108,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   if (CL > 1) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = hdr->tmem_base;
-  constexpr uint32_t kIdesc = make_idesc(2, 1, 128, 128);
+  constexpr uint32_t kIdesc = kI8 ? make_idesc(2, 1, 128, 128)
+                                  : (KIND == TcKind::BF16 ? make_idesc(1, 1, 128, 128) : make_idesc(1, 0, 128, 128));
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         const int vl = doc_valid_len(p, b);
         const int ntiles = (vl + kTileRows - 1) / kTileRows;
         for (int t = 0; t < ntiles; ++t) {
-          {
+          if constexpr (kI8) {
             const int ss = (int)(sc_n % kScaleSlots);
             mbar_wait_idle(&hdr->sempty[ss], ((sc_n / kScaleSlots) & 1u) ^ 1u);
             const uint32_t bytes = (uint32_t)min(kTileRows, p.l_pad - t * kTileRows) * 4u;
@@ -125,13 +133,16 @@ __global__ void __launch_bounds__(kR8Threads, 1)
             ++sc_n;
           }
           mbar_wait_idle(&hdr->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)kAtomBytes);
+          mbar_arrive_expect_tx(&hdr->full[stage], (uint32_t)(KA * kAtomBytes));
           const int row0 = b * p.l_pad + t * kTileRows + crank * kRowsPer;
-          uint8_t* dst = sD + (size_t)stage * kAtomBytes + crank * kRowsPer * 128;
-          if (CL > 1)
-            tma_load_2d_mc(&tmD, &hdr->full[stage], dst, 0, row0, kMask, kEvictFirst);
-          else
-            tma_load_2d(&tmD, &hdr->full[stage], dst, 0, row0, kEvictFirst);
+#pragma unroll
+          for (int a = 0; a < KA; ++a) {
+            uint8_t* dst = sD + (size_t)(stage * KA + a) * kAtomBytes + crank * kRowsPer * 128;
+            if (CL > 1)
+              tma_load_2d_mc(&tmD, &hdr->full[stage], dst, a * kElemsPerAtom, row0, kMask, kEvictFirst);
+            else
+              tma_load_2d(&tmD, &hdr->full[stage], dst, a * kElemsPerAtom, row0, kEvictFirst);
+          }
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
@@ -166,7 +177,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       for (int t = 0; t < ntiles; ++t) {
         mbar_wait_idle(&hdr->full[stage], phase);
         tc_fence_after();
-        const uint64_t bd0 = ddesc0 + (uint64_t)((stage * kAtomBytes) >> 4);
+        const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
         for (int mb = 0; mb < qbv; ++mb, ++nblk) {
           const uint32_t slot = nblk % kR8Sets, use = nblk / kR8Sets;
           mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
@@ -175,8 +186,13 @@ __global__ void __launch_bounds__(kR8Threads, 1)
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
             const uint32_t dcol = tmem_base + (uint32_t)(kR8AccCol0 + slot * 128);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_i8_ts(dcol, acol + k * 8, bd0 + (uint64_t)((k * 32) >> 4), kIdesc, k > 0 ? 1u : 0u);
+            for (int k = 0; k < KA * 4; ++k) {
+              const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
+              if constexpr (kI8)
+                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+              else
+                mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+            }
             mma_commit(&hdr->tfull[slot]);
           }
           __syncwarp();
@@ -214,20 +230,25 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           qeph ^= 1;
         }
         // Q block mb is written by set mb % 3 (each warp its quadrant's 32 rows)
+        const int row_bytes = p.dim * (kI8 ? 1 : 2);
         for (int mb = set; mb < qbv; mb += kR8Sets) {
           const int row = (g * p.qb + mb) * kTileRows + row_local;
-          const uint8_t* src = static_cast<const uint8_t*>(p.q_ptr) + ((long long)q * p.l_q + row) * p.dim;
-          uint32_t r[32];
+          const uint8_t* src = static_cast<const uint8_t*>(p.q_ptr) + ((long long)q * p.l_q + row) * row_bytes;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            uint4 w = make_uint4(0u, 0u, 0u, 0u);
-            if (row < p.l_q && c * 16 < p.dim) w = __ldg(reinterpret_cast<const uint4*>(src + c * 16));
-            r[4 * c] = w.x;
-            r[4 * c + 1] = w.y;
-            r[4 * c + 2] = w.z;
-            r[4 * c + 3] = w.w;
+          for (int a = 0; a < KA; ++a) {
+            uint32_t r[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int off = a * 128 + c * 16;
+              uint4 w = make_uint4(0u, 0u, 0u, 0u);
+              if (row < p.l_q && off < row_bytes) w = __ldg(reinterpret_cast<const uint4*>(src + off));
+              r[4 * c] = w.x;
+              r[4 * c + 1] = w.y;
+              r[4 * c + 2] = w.z;
+              r[4 * c + 3] = w.w;
+            }
+            tmem_st32(tmem_base + lane_base + (uint32_t)(mb * kQCols + a * 32), r);
           }
-          tmem_st32(tmem_base + lane_base + (uint32_t)(mb * kQCols), r);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -242,12 +263,12 @@ __global__ void __launch_bounds__(kR8Threads, 1)
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) {
         const int row = (g * p.qb + mb) * kTileRows + row_local;
-        sq[mb] = (mb < qbv && row < p.l_q) ? __ldg(p.q_scale + (long long)q * p.l_q + row) : 1.f;
+        sq[mb] = (kI8 && mb < qbv && row < p.l_q) ? __ldg(p.q_scale + (long long)q * p.l_q + row) : 1.f;
       }
       for (int t = 0; t < ntiles; ++t) {
         const int ss = (int)(sc_n % kScaleSlots);
-        mbar_wait(&hdr->sfull[ss], (sc_n / kScaleSlots) & 1u);
-        const float* sdt = sScale + ss * kTileRows;
+        if constexpr (kI8) mbar_wait(&hdr->sfull[ss], (sc_n / kScaleSlots) & 1u);
+        const float* sdt = kI8 ? sScale + ss * kTileRows : nullptr;
         const int base = t * kTileRows;
         const bool full = base + kTileRows <= vl;
         // this set's blocks of the tile (one or two of the four); a rolled loop keeps the code
@@ -266,11 +287,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           tmem_ld32(taddr + 32, rb);
           tmem_ld_wait();
           if (full) {
-            ts_chunk_full<TcKind::I8, false>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
-            ts_chunk_full<TcKind::I8, false>(rb, base + 32, sqm, pm, cbd, nullptr, 0, sdt + 32);
+            ts_chunk_full<KIND, false>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk_full<KIND, false>(rb, base + 32, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
           } else {
-            ts_chunk<TcKind::I8, true>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
-            ts_chunk<TcKind::I8, true>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 32);
+            ts_chunk<KIND, true>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk<KIND, true>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
           }
           tmem_ld32(taddr + 64, ra);
           tmem_ld32(taddr + 96, rb);
@@ -279,11 +300,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&hdr->tempty[set]);
           if (full) {
-            ts_chunk_full<TcKind::I8, false>(ra, base + 64, sqm, pm, cbd, nullptr, 0, sdt + 64);
-            ts_chunk_full<TcKind::I8, false>(rb, base + 96, sqm, pm, cbd, nullptr, 0, sdt + 96);
+            ts_chunk_full<KIND, false>(ra, base + 64, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
+            ts_chunk_full<KIND, false>(rb, base + 96, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           } else {
-            ts_chunk<TcKind::I8, true>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 64);
-            ts_chunk<TcKind::I8, true>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt + 96);
+            ts_chunk<KIND, true>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
+            ts_chunk<KIND, true>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           }
           part[0] = mb == 0 ? pm : part[0];
           part[1] = mb == 1 ? pm : part[1];
@@ -291,8 +312,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           part[3] = mb == 3 ? pm : part[3];
         }
         nblk += (uint32_t)qbv;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&hdr->sempty[ss]);
+        if constexpr (kI8) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hdr->sempty[ss]);
+        }
         ++sc_n;
       }
       // ---- combine the three sets' partial maxima of this document (double-buffered by parity)

@@ -438,6 +438,21 @@ def test_contrastive_drift_api():
     assert out["loss_last_fused"] < out["loss_first"]
 
 
+@pytest.mark.parametrize("l_q", [200, 512, 1024])
+def test_rerank_three_slot_kernel_matches(l_q, monkeypatch):
+    """The opt-in three-slot rerank kernel (MXS_RERANK_IMPL=r3; 2 resident Q blocks, 4-CTA
+    clusters at L_q = 1024) returns the same score bits as the default forward."""
+    rng = np.random.default_rng(l_q)
+    Q = cuda(orc.make_queries(1, l_q, 128, seed=5), torch.bfloat16)
+    lens = rng.integers(1, 300, 160).astype(np.int32)
+    D, vl = orc.padded(orc.make_corpus(160, lens, 128, seed=6), 300)
+    Dt, vlt = cuda(D, torch.bfloat16), cuda(vl)
+    s_ts, _, _ = mx.score_dense(Q, Dt, vlt, want_argmax=False)
+    monkeypatch.setenv("MXS_RERANK_IMPL", "r3")
+    s_r3, _, _ = mx.score_dense(Q, Dt, vlt, want_argmax=False)
+    assert torch.equal(s_ts, s_r3)
+
+
 def test_scores_without_argmax_are_identical():
     """The rerank mode (argmax not requested: max only, no index tracking) returns the same bits."""
     rng = np.random.default_rng(17)
