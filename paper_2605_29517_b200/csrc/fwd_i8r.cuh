@@ -42,10 +42,26 @@ struct R8SmemHeader {
 };
 
 // dynamic smem: document tiles + per-document partial maxima [2 docs][3 sets][4 blocks][128 rows]
-// + the scale ring
+// + the scale ring + the INT8 bias tile (one SW128 K-major bf16 atom, 128 rows x 128 B)
+constexpr int kR8BiasBytes = 128 * 128;
 __host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages) {
   return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
-         (size_t)kScaleSlots * kTileRows * sizeof(float);
+         (size_t)kScaleSlots * kTileRows * sizeof(float) + kR8BiasBytes;
+}
+
+// INT8 accumulators start from the f32 bits of kMagicF instead of zero, so the epilogue's exact
+// s32 -> f32 is one FADD2 per pair (i2f2_biased) rather than two IADDs and an FADD2 -- a third of
+// the issue slots of the issue-bound INT8 epilogue.  The bias is written by the tensor core, not
+// by tcgen05.st: one kind::f16 MMA (enable_input_d = 0) of a constant bf16 tile against itself,
+// K = 16, every 16-byte chunk of which is {2048, 1024, 1024, 0, 0, 0, 0, 0}, so each output is
+// 2 * (2^22 + 2^20 + 2^20) = 1.5 * 2^23 exactly -- the f32 kMagicF whose bits are kMagicI2F --
+// whatever the swizzle.  The kind::i8 MMAs then accumulate (s32, enable_input_d = 1) on top:
+// TMEM = kMagicI2F + acc, |acc| <= 2^21 for d <= 128.  Cost: one K = 16 bf16 MMA per accumulator
+// (+25 % tensor-pipe time on an epilogue-bound kernel).
+MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
+  const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
+  uint4* t4 = reinterpret_cast<uint4*>(tile);
+  for (int i = tid; i < kR8BiasBytes / 16; i += nthreads) t4[i] = chunk;
 }
 
 template <TcKind KIND, int KA, int CL>
@@ -57,6 +73,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   uint8_t* sD = smem;
   float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
   float* sScale = sPart + (size_t)2 * kR8Sets * 4 * 128;
+  uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + kScaleSlots * kTileRows);  // 1024-B aligned
   __shared__ R8SmemHeader r8_hdr;
   R8SmemHeader* hdr = &r8_hdr;
 
@@ -103,6 +120,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
+  if constexpr (KIND == TcKind::I8) {
+    fill_bias_tile(sBias, (int)threadIdx.x, kR8Threads);
+    fence_proxy_async();  // generic-proxy writes -> tensor-core (async proxy) reads
+  }
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();
@@ -157,6 +178,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     uint32_t nblk = 0;  // accumulators produced so far: slot = nblk % 3
     long long cur_key = -1;
     const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
+    const uint64_t bias_desc = sw128_kmajor_desc(smem_u32(sBias));
+    constexpr uint32_t kBiasIdesc = make_idesc(1, 1, 128, 128);  // f32 <- bf16 x bf16
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
       decode(u, q, g, b);
@@ -185,11 +208,12 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
             const uint32_t dcol = tmem_base + (uint32_t)(kR8AccCol0 + slot * 128);
+            if constexpr (kI8) mma_f16_ss(dcol, bias_desc, bias_desc, kBiasIdesc, 0u);  // TMEM = kMagicF
 #pragma unroll
             for (int k = 0; k < KA * 4; ++k) {
               const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
               if constexpr (kI8)
-                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, 1u);
               else
                 mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
             }
@@ -287,11 +311,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           tmem_ld32(taddr + 32, rb);
           tmem_ld_wait();
           if (full) {
-            ts_chunk_full<KIND, false>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
-            ts_chunk_full<KIND, false>(rb, base + 32, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
+            ts_chunk_full<KIND, false, kI8>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk_full<KIND, false, kI8>(rb, base + 32, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
           } else {
-            ts_chunk<KIND, true>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
-            ts_chunk<KIND, true>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
+            ts_chunk<KIND, true, kI8>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk<KIND, true, kI8>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
           }
           tmem_ld32(taddr + 64, ra);
           tmem_ld32(taddr + 96, rb);
@@ -300,11 +324,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&hdr->tempty[set]);
           if (full) {
-            ts_chunk_full<KIND, false>(ra, base + 64, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
-            ts_chunk_full<KIND, false>(rb, base + 96, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
+            ts_chunk_full<KIND, false, kI8>(ra, base + 64, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
+            ts_chunk_full<KIND, false, kI8>(rb, base + 96, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           } else {
-            ts_chunk<KIND, true>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
-            ts_chunk<KIND, true>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
+            ts_chunk<KIND, true, kI8>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
+            ts_chunk<KIND, true, kI8>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           }
           part[0] = mb == 0 ? pm : part[0];
           part[1] = mb == 1 ? pm : part[1];

@@ -62,7 +62,7 @@ MXS_DEV void unstash_chunk(const float* row128, float (&v)[32], int swz) {
   }
 }
 
-template <TcKind KIND, bool kMagic = false>
+template <TcKind KIND, bool kMagic = false, bool kBiased = false>
 MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcParams& p, int b, float sq, float& m,
                       int& cb, float* stash_row, int swz, const float* sd_smem = nullptr) {
   if (base >= vl) return;
@@ -103,7 +103,9 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
 #pragma unroll
     for (int j = 0; j < 32; j += 2) {
       float c0, c1, t0, t1;
-      if constexpr (kMagic) {
+      if constexpr (kBiased) {
+        i2f2_biased(c0, c1, r[j], r[j + 1]);
+      } else if constexpr (kMagic) {
         i2f2_magic(c0, c1, r[j], r[j + 1]);
       } else {
         c0 = __int2float_rn((int)r[j]);
@@ -139,7 +141,7 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
 // Fast path of ts_chunk for a chunk that lies entirely inside the document (no masking), with
 // the INT8 scales already in shared memory and the argmax decision made at compile time: no
 // per-chunk bounds checks or pointer tests, so the compiler sees one straight-line block.
-template <TcKind KIND, bool kArgmax>
+template <TcKind KIND, bool kArgmax, bool kBiased = false>
 MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m, int& cb, float* stash_row, int swz,
                            const float* sd_smem) {
   float v[32];
@@ -149,8 +151,13 @@ MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m
     for (int c = 0; c < 8; ++c) {
       const float4 t = s4[c];
       float c0, c1, c2, c3, t0, t1, t2, t3;
-      i2f2_magic(c0, c1, r[4 * c], r[4 * c + 1]);
-      i2f2_magic(c2, c3, r[4 * c + 2], r[4 * c + 3]);
+      if constexpr (kBiased) {
+        i2f2_biased(c0, c1, r[4 * c], r[4 * c + 1]);
+        i2f2_biased(c2, c3, r[4 * c + 2], r[4 * c + 3]);
+      } else {
+        i2f2_magic(c0, c1, r[4 * c], r[4 * c + 1]);
+        i2f2_magic(c2, c3, r[4 * c + 2], r[4 * c + 3]);
+      }
       fmul2_rn(t0, t1, c0, c1, sq, sq);
       fmul2_rn(t2, t3, c2, c3, sq, sq);
       fmul2_rn(v[4 * c], v[4 * c + 1], t0, t1, t.x, t.y);

@@ -271,6 +271,11 @@ constexpr float kMagicF = 12582912.0f;  // 1.5 * 2^23
 MXS_DEV void i2f2_magic(float& o0, float& o1, uint32_t a0, uint32_t a1) {
   fadd2_rn(o0, o1, __int_as_float((int)a0 + kMagicI2F), __int_as_float((int)a1 + kMagicI2F), -kMagicF, -kMagicF);
 }
+// The same conversion when the s32 accumulator was pre-loaded with the bits of kMagicF (TMEM then
+// holds kMagicI2F + acc, i.e. the f32 value kMagicF + acc): one FADD2, no integer add.
+MXS_DEV void i2f2_biased(float& o0, float& o1, uint32_t a0, uint32_t a1) {
+  fadd2_rn(o0, o1, __uint_as_float(a0), __uint_as_float(a1), -kMagicF, -kMagicF);
+}
 MXS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
