@@ -281,7 +281,8 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   }
   const size_t max_smem = 232448 - sizeof(mxs::TsSmemHeader);  // static header comes out of the same 227 KB
   const bool scale_ring = (KIND == mxs::TcKind::I8) && (l_pad % 4 == 0);
-  const size_t fixed = mxs::fwd_ts_smem_bytes(0, qb, 0, scale_ring);
+  const bool bias = (KIND == mxs::TcKind::I8) && ka <= 2;  // fwd_ts_kernel's kBias
+  const size_t fixed = mxs::fwd_ts_smem_bytes(0, qb, 0, scale_ring, bias);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
@@ -312,7 +313,7 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
                                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   int s;
   if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
-  const size_t smem = mxs::fwd_ts_smem_bytes(ka, qb, stages, scale_ring);
+  const size_t smem = mxs::fwd_ts_smem_bytes(ka, qb, stages, scale_ring, bias);
   using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
   KernT kern = nullptr;
 #define MXS_TS_CASE(KA_, CL_) \

@@ -42,26 +42,10 @@ struct R8SmemHeader {
 };
 
 // dynamic smem: document tiles + per-document partial maxima [2 docs][3 sets][4 blocks][128 rows]
-// + the scale ring + the INT8 bias tile (one SW128 K-major bf16 atom, 128 rows x 128 B)
-constexpr int kR8BiasBytes = 128 * 128;
+// + the scale ring + the INT8 bias tile
 __host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages) {
   return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
-         (size_t)kScaleSlots * kTileRows * sizeof(float) + kR8BiasBytes;
-}
-
-// INT8 accumulators start from the f32 bits of kMagicF instead of zero, so the epilogue's exact
-// s32 -> f32 is one FADD2 per pair (i2f2_biased) rather than two IADDs and an FADD2 -- a third of
-// the issue slots of the issue-bound INT8 epilogue.  The bias is written by the tensor core, not
-// by tcgen05.st: one kind::f16 MMA (enable_input_d = 0) of a constant bf16 tile against itself,
-// K = 16, every 16-byte chunk of which is {2048, 1024, 1024, 0, 0, 0, 0, 0}, so each output is
-// 2 * (2^22 + 2^20 + 2^20) = 1.5 * 2^23 exactly -- the f32 kMagicF whose bits are kMagicI2F --
-// whatever the swizzle.  The kind::i8 MMAs then accumulate (s32, enable_input_d = 1) on top:
-// TMEM = kMagicI2F + acc, |acc| <= 2^21 for d <= 128.  Cost: one K = 16 bf16 MMA per accumulator
-// (+25 % tensor-pipe time on an epilogue-bound kernel).
-MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
-  const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
-  uint4* t4 = reinterpret_cast<uint4*>(tile);
-  for (int i = tid; i < kR8BiasBytes / 16; i += nthreads) t4[i] = chunk;
+         (size_t)kScaleSlots * kTileRows * sizeof(float) + kBiasTileBytes;
 }
 
 template <TcKind KIND, int KA, int CL>

@@ -37,10 +37,28 @@ struct TsSmemHeader {
   uint32_t pad;
 };
 
-// dynamic shared memory (the header is static shared memory); `scales` adds the INT8 scale ring
-__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales = false) {
+// INT8 accumulators start from the f32 bits of kMagicF instead of zero, so the epilogue's exact
+// s32 -> f32 is one FADD2 per pair (i2f2_biased) rather than two IADDs and an FADD2 -- a third of
+// the issue slots of the issue-bound INT8 epilogue.  The bias is written by the tensor core, not
+// by tcgen05.st: one kind::f16 MMA (enable_input_d = 0) of a constant bf16 tile against itself,
+// K = 16, every 16-byte chunk of which is {2048, 1024, 1024, 0, 0, 0, 0, 0}, so each output is
+// 2 * (2^22 + 2^20 + 2^20) = 1.5 * 2^23 exactly -- the f32 kMagicF whose bits are kMagicI2F --
+// whatever the swizzle.  The kind::i8 MMAs then accumulate (s32, enable_input_d = 1) on top:
+// TMEM = kMagicI2F + acc, |acc| <= 2^21 for d <= 128.  Cost: one K = 16 bf16 MMA per accumulator
+// (+25 % tensor-pipe time on an epilogue-bound kernel).
+constexpr int kBiasTileBytes = 128 * 128;  // one SW128 K-major bf16 atom, 128 rows x 128 B
+MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
+  const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
+  uint4* t4 = reinterpret_cast<uint4*>(tile);
+  for (int i = tid; i < kBiasTileBytes / 16; i += nthreads) t4[i] = chunk;
+}
+
+
+// dynamic shared memory (the header is static shared memory); `scales` adds the INT8 scale ring,
+// `bias` the ring's space (used or not) plus the INT8 bias tile after it
+__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales = false, bool bias = false) {
   return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128 +
-         (scales ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0);
+         ((scales || bias) ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0) + (bias ? kBiasTileBytes : 0);
 }
 
 // Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
@@ -194,6 +212,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   // INT8 scale ring (only when d_scale rows are 16-B aligned: l_pad % 4 == 0)
   float* sScale = sBest + (size_t)p.qb * 128 * 32;
   const bool scale_ring = (KIND == TcKind::I8) && ((p.l_pad & 3) == 0);
+  // INT8 with |acc| <= 2^22 (d <= 256): accumulators pre-biased to kMagicF (see fill_bias_tile)
+  constexpr bool kBias = (KIND == TcKind::I8) && (KA <= 2);
+  uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + kScaleSlots * kTileRows);
   __shared__ TsSmemHeader ts_hdr;  // static shared: keeps barrier / bookkeeping accesses on LDS/STS
   TsSmemHeader* hdr = &ts_hdr;
 
@@ -239,6 +260,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
+  if constexpr (kBias) {
+    fill_bias_tile(sBias, (int)threadIdx.x, kTsThreads);
+    fence_proxy_async();
+  }
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();
@@ -300,6 +325,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     uint32_t sbits = 0;  // bit s = parity of slot s's next use
     long long cur_key = -1;
     const uint64_t ddesc0 = sw128_kmajor_desc(smem_u32(sD));
+    const uint64_t bias_desc = sw128_kmajor_desc(smem_u32(sBias));
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
       decode(u, q, g, b);
@@ -328,11 +354,12 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
             const uint32_t dcol = tmem_base + (uint32_t)(kTsAccCol0 + slot * 128);
+            if constexpr (kBias) mma_f16_ss(dcol, bias_desc, bias_desc, make_idesc(1, 1, 128, 128), 0u);
 #pragma unroll
             for (int k = 0; k < KA * 4; ++k) {
               const uint64_t koff = (uint64_t)(((k >> 2) * kAtomBytes + (k & 3) * 32) >> 4);
               if constexpr (KIND == TcKind::I8)
-                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
+                mma_i8_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, (kBias || k > 0) ? 1u : 0u);
               else
                 mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
             }
@@ -450,11 +477,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tmem_ld32(taddr + 32, rb);
             tmem_ld_wait();
             if (stash) {
-              ts_chunk_full<KIND, true>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
-              ts_chunk_full<KIND, true>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
+              ts_chunk_full<KIND, true, kBias>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
+              ts_chunk_full<KIND, true, kBias>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
             } else {
-              ts_chunk_full<KIND, false>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
-              ts_chunk_full<KIND, false>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
+              ts_chunk_full<KIND, false, kBias>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
+              ts_chunk_full<KIND, false, kBias>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
             }
             tmem_ld32(taddr + 64, ra);
             tmem_ld32(taddr + 96, rb);
@@ -463,11 +490,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
             if (stash) {
-              ts_chunk_full<KIND, true>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
-              ts_chunk_full<KIND, true>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
+              ts_chunk_full<KIND, true, kBias>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
+              ts_chunk_full<KIND, true, kBias>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
             } else {
-              ts_chunk_full<KIND, false>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
-              ts_chunk_full<KIND, false>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
+              ts_chunk_full<KIND, false, kBias>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
+              ts_chunk_full<KIND, false, kBias>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
             }
           } else if constexpr (KIND == TcKind::I8) {
             // the dequantisation needs extra registers: two chunks in flight at a time
@@ -475,16 +502,16 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tmem_ld32(taddr, ra);
             tmem_ld32(taddr + 32, rb);
             tmem_ld_wait();
-            ts_chunk<KIND, (KA <= 2)>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt);
-            ts_chunk<KIND, (KA <= 2)>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 32 : sdt);
+            ts_chunk<KIND, (KA <= 2), kBias>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt);
+            ts_chunk<KIND, (KA <= 2), kBias>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 32 : sdt);
             tmem_ld32(taddr + 64, ra);
             tmem_ld32(taddr + 96, rb);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
-            ts_chunk<KIND, (KA <= 2)>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 64 : sdt);
-            ts_chunk<KIND, (KA <= 2)>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 96 : sdt);
+            ts_chunk<KIND, (KA <= 2), kBias>(ra, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 64 : sdt);
+            ts_chunk<KIND, (KA <= 2), kBias>(rb, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz, sdt ? sdt + 96 : sdt);
           } else if (KIND != TcKind::I8 && base + kTileRows <= vl) {
             uint32_t ra[32], rb[32], rc[32], rd[32];
             tmem_ld32(taddr, ra);
@@ -496,15 +523,15 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
             if (stash) {
-              ts_chunk_full<KIND, true>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, true>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, true>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, true>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true, kBias>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true, kBias>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true, kBias>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, true, kBias>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
             } else {
-              ts_chunk_full<KIND, false>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, false>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, false>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
-              ts_chunk_full<KIND, false>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false, kBias>(ra, base, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false, kBias>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false, kBias>(rc, base + 64, sq[i], m[i], cb[i], stash, swz, nullptr);
+              ts_chunk_full<KIND, false, kBias>(rd, base + 96, sq[i], m[i], cb[i], stash, swz, nullptr);
             }
           } else {
             uint32_t ra[32], rb[32], rc[32], rd[32];
@@ -516,10 +543,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
-            ts_chunk<KIND, (KA <= 2)>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND, (KA <= 2)>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND, (KA <= 2)>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
-            ts_chunk<KIND, (KA <= 2)>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2), kBias>(ra, base, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2), kBias>(rb, base + 32, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2), kBias>(rc, base + 64, vl, p, b, sq[i], m[i], cb[i], stash, swz);
+            ts_chunk<KIND, (KA <= 2), kBias>(rd, base + 96, vl, p, b, sq[i], m[i], cb[i], stash, swz);
           }
         }
         if (scale_ring) {  // this warp is done with the tile's scales

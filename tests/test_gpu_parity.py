@@ -239,6 +239,30 @@ def test_int8_random_bitwise_incl_ties(l_q, n_docs, l_pad, dim):
     assert am2 is None and np.array_equal(sc2.cpu().numpy(), ref_s)
 
 
+@pytest.mark.parametrize("dim", [128, 256, 384])
+def test_int8_extreme_accumulators_bitwise(dim):
+    """Raw int8 at the edges of the s32 range the kernels convert: all -128 x -128 at d = 256 gives
+    acc = 2^22 exactly (the limit of the biased / magic-number s32 -> f32), -128 x 127 the most
+    negative sums; d = 384 takes the cvt path.  Scores and argmax bit-identical to the oracle."""
+    rng = np.random.default_rng(dim)
+    l_q, n_docs, l_pad = 160, 6, 256
+    qq = rng.integers(-128, 128, (1, l_q, dim)).astype(np.int8)
+    dq = rng.integers(-128, 128, (n_docs, l_pad, dim)).astype(np.int8)
+    qq[0, :40] = -128
+    dq[0] = -128            # acc = dim * 2^14 for the first 40 query rows
+    dq[1] = 127             # acc = -dim * 128 * 127
+    dq[2, ::3] = -128
+    qs = rng.uniform(0.001, 0.05, (1, l_q)).astype(np.float32)
+    ds = rng.uniform(0.001, 0.05, (n_docs, l_pad)).astype(np.float32)
+    lens = np.array([256, 255, 129, 128, 1, 77], dtype=np.int32)
+    sc, am, _ = mx.score_int8(cuda(qq), cuda(qs), cuda(dq), cuda(ds), cuda(lens))
+    ref_s, ref_a = orc.fused_score_int8(qq, qs, dq, ds, lens)
+    assert np.array_equal(sc.cpu().numpy(), ref_s)
+    assert np.array_equal(am.cpu().numpy(), ref_a)
+    sc2, _, _ = mx.score_int8(cuda(qq), cuda(qs), cuda(dq), cuda(ds), cuda(lens), want_argmax=False)
+    assert np.array_equal(sc2.cpu().numpy(), ref_s)
+
+
 def test_two_stage_topk_matches_reference():
     g = golden("two_stage")
     D = g["D"]
