@@ -59,6 +59,14 @@ t_bf = timeit(lambda: mx.score_dense(Qf, Df, want_argmax=False))
 t_bfa = timeit(lambda: mx.score_dense(Qf, Df))
 print(f"C4 int8 rerank {t_i8:.3f} ms ({nb / t_i8 * 1e3 / 1e6:.2f} M docs/s, {2.684e12 / t_i8 / 1e9:.0f} TOP/s), "
       f"+argmax {t_i8a:.3f} ms | bf16 rerank {t_bf:.3f} ms, +argmax {t_bfa:.3f} ms | quantize corpus {t_q:.3f} ms")
+# measured INT8 dense peak (torch._int_mm at 8192^3, the cuBLASLt s8 x s8 -> s32 GEMM)
+a8 = torch.randint(-127, 128, (8192, 8192), dtype=torch.int8, device="cuda")
+b8 = torch.randint(-127, 128, (8192, 8192), dtype=torch.int8, device="cuda").t()
+t_mm = timeit(lambda: torch._int_mm(a8, b8), reps=10, warm=3)
+peak8 = 2 * 8192 ** 3 / t_mm / 1e9
+print(f"C4 roofline: int8 peak (torch._int_mm 8192^3) {peak8:.0f} TOP/s; rerank kernel {2.684e12 / t_i8 / 1e9:.0f} TOP/s "
+      f"= {2.684e12 / t_i8 / 1e9 / peak8:.1%} of measured, {2.684e12 / t_i8 / 1e9 / 4500:.1%} of 4.5 POPS spec")
+del a8, b8
 del Df, dq
 
 # C5 scaled: varlen 100K docs L in [32, 512], L_q = 32
