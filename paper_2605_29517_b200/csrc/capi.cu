@@ -204,7 +204,7 @@ int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   const int n_groups = (nmb + qb - 1) / qb;
   const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
   const size_t max_smem = 232448 - sizeof(mxs::R8SmemHeader);
-  const size_t fixed = mxs::fwd_i8r_smem_bytes(ka, 0);
+  const size_t fixed = mxs::fwd_i8r_smem_bytes(ka, 0, kI8);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
@@ -231,7 +231,7 @@ int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   CUtensorMap td;
   int s;
   if ((s = make_tmap_2d(&td, D, dt, eb, dim, n_docs * l_pad, 128 / cl)) != MXS_OK) return s;
-  const size_t smem = mxs::fwd_i8r_smem_bytes(ka, stages);
+  const size_t smem = mxs::fwd_i8r_smem_bytes(ka, stages, kI8);
   using KernT = void (*)(const CUtensorMap, const mxs::FwdTcParams);
   KernT kern = cl == 4   ? mxs::fwd_i8r_kernel<KIND, ka, 4>
                : cl == 2 ? mxs::fwd_i8r_kernel<KIND, ka, 2>

@@ -28,7 +28,11 @@ constexpr int kR8EpiWarps = 4 * kR8Sets;
 constexpr int kR8Threads = 32 * (2 + kR8EpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM, 2..13 epilogue
 constexpr int kR8AccCol0 = 128;
 
+constexpr int kR8PartBufs = 4;  // per-document partial-maximum buffers in flight
+
 struct R8SmemHeader {
+  uint32_t pcnt[kR8PartBufs][4];  // sets (warps) of a quadrant that have published doc partials
+  uint32_t pgen[kR8PartBufs][4];  // documents combined out of this buffer so far
   uint64_t full[8];
   uint64_t empty[8];
   uint64_t tfull[kR8Sets];
@@ -41,11 +45,11 @@ struct R8SmemHeader {
   uint32_t pad;
 };
 
-// dynamic smem: document tiles + per-document partial maxima [2 docs][3 sets][4 blocks][128 rows]
-// + the scale ring + the INT8 bias tile
-__host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)2 * kR8Sets * 4 * 128 * sizeof(float) +
-         (size_t)kScaleSlots * kTileRows * sizeof(float) + kBiasTileBytes;
+// dynamic smem: document tiles + per-document partial maxima [4 docs][3 sets][4 blocks][128 rows]
+// + (INT8) the scale ring and the bias tile
+__host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages, bool i8) {
+  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)kR8PartBufs * kR8Sets * 4 * 128 * sizeof(float) +
+         (i8 ? (size_t)kScaleSlots * kTileRows * sizeof(float) + kBiasTileBytes : 0);
 }
 
 template <TcKind KIND, int KA, int CL>
@@ -56,7 +60,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sD = smem;
   float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
-  float* sScale = sPart + (size_t)2 * kR8Sets * 4 * 128;
+  float* sScale = sPart + (size_t)kR8PartBufs * kR8Sets * 4 * 128;
   uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + kScaleSlots * kTileRows);  // 1024-B aligned
   __shared__ R8SmemHeader r8_hdr;
   R8SmemHeader* hdr = &r8_hdr;
@@ -102,6 +106,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       mbar_init(&hdr->sempty[s], kR8EpiWarps);
     }
     fence_mbar_init();
+  }
+  if (threadIdx.x < kR8PartBufs * 4) {
+    (&hdr->pcnt[0][0])[threadIdx.x] = 0u;
+    (&hdr->pgen[0][0])[threadIdx.x] = 0u;
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
   if constexpr (KIND == TcKind::I8) {
@@ -326,18 +334,39 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         }
         ++sc_n;
       }
-      // ---- combine the three sets' partial maxima of this document (double-buffered by parity)
-      float* buf = sPart + (size_t)(ndoc & 1u) * kR8Sets * 4 * 128;
+      // ---- combine the three sets' partial maxima of this document without a barrier: every warp
+      // publishes its partials into the document's buffer and counts itself in; the last of the
+      // three warps of a quadrant (one per set) max-combines the quadrant's rows and writes them.
+      // A set can run several documents ahead of another (small documents), so a buffer is only
+      // re-filled once its previous document has been combined (generation check, rarely waits).
+      const uint32_t pb = ndoc % kR8PartBufs, gen = ndoc / kR8PartBufs;
+      volatile uint32_t* pgen = &hdr->pgen[pb][quad];
+      while (*pgen != gen) {
+      }
+      float* buf = sPart + (size_t)pb * kR8Sets * 4 * 128;
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) buf[(set * 4 + mb) * 128 + row_local] = part[mb];
-      named_bar_sync(1, 32 * kR8EpiWarps);
-      // set s writes out blocks mb with mb % 3 == s
-      const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
-      for (int mb = set; mb < qbv; mb += kR8Sets) {
-        const int row = (g * p.qb + mb) * kTileRows + row_local;
-        const float m = fmaxf(fmaxf(buf[(0 * 4 + mb) * 128 + row_local], buf[(1 * 4 + mb) * 128 + row_local]),
-                              buf[(2 * 4 + mb) * 128 + row_local]);
-        if (row < p.l_q) p.rowmax[obase + row] = m;
+      __threadfence_block();
+      __syncwarp();
+      uint32_t arrived = 0;
+      if (lane == 0) arrived = atomicAdd(&hdr->pcnt[pb][quad], 1u);
+      arrived = __shfl_sync(0xffffffffu, arrived, 0);
+      if (arrived == kR8Sets - 1) {
+        __threadfence_block();
+        const volatile float* vb = buf;
+        const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
+        for (int mb = 0; mb < qbv; ++mb) {
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          const float m = fmaxf(fmaxf(vb[(0 * 4 + mb) * 128 + row_local], vb[(1 * 4 + mb) * 128 + row_local]),
+                                vb[(2 * 4 + mb) * 128 + row_local]);
+          if (row < p.l_q) p.rowmax[obase + row] = m;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          hdr->pcnt[pb][quad] = 0u;
+          __threadfence_block();
+          *pgen = gen + 1u;
+        }
       }
       ++ndoc;
     }
