@@ -157,6 +157,8 @@ int launch_fwd_tc(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   {
     const char* dbg = getenv("MXS_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
+    const char* spin = getenv("MXS_MMA_SPIN");
+    p.mma_spin = spin ? atoi(spin) : 0;
   }
   CUtensorMap tq, td;
   const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
@@ -225,6 +227,10 @@ int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   p.rowmax = rowmax;
   p.argmax = nullptr;
   p.q_ptr = Q;
+  {
+    const char* dbg = getenv("MXS_DEBUG");  // 3 (bf16/fp16): MMA never waits for the drain
+    p.debug = (dbg && !kI8) ? atoi(dbg) : 0;
+  }
   const CUtensorMapDataType dt = kI8                         ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : KIND == mxs::TcKind::BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -306,6 +312,8 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   {
     const char* dbg = getenv("MXS_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
+    const char* spin = getenv("MXS_MMA_SPIN");
+    p.mma_spin = spin ? atoi(spin) : 0;
   }
   CUtensorMap td;
   const CUtensorMapDataType dt = (KIND == mxs::TcKind::I8)     ? CU_TENSOR_MAP_DATA_TYPE_UINT8

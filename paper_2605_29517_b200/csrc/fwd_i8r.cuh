@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
         for (int mb = 0; mb < qbv; ++mb, ++nblk) {
           const uint32_t slot = nblk % kR8Sets, use = nblk / kR8Sets;
-          mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
+          if (p.debug != 3) mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
@@ -225,6 +225,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           phase ^= 1;
         }
       }
+    }
+    if (p.debug == 3) {  // nobody drained: wait for the last MMAs before TMEM is freed
+      if (elect_one()) mma_commit(&hdr->qempty);
+      __syncwarp();
+      mbar_wait(&hdr->qempty, qphase ^ 1u);
     }
   } else {
     // ------------------------------------------------------------------ epilogue sets
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         if (lane == 0) mbar_arrive(&hdr->qfull);
         cur_key = key;
       }
+      if (!kI8 && p.debug == 3) continue;  // profiling: no drain, no output
       const int vl = doc_valid_len(p, b);
       const int ntiles = (vl + kTileRows - 1) / kTileRows;
       float part[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};

@@ -34,6 +34,7 @@ struct FwdTcParams {
   float* rowmax;              // [n_q, n_docs, l_q]
   int32_t* argmax;            // [n_q, n_docs, l_q] or nullptr
   int debug;                  // profiling knobs (MXS_DEBUG env): 1 = skip fold, 2 = skip TMEM loads too
+  int mma_spin;               // MXS_MMA_SPIN=1: the MMA issuer spins (no suspend) on accumulator-slot waits
   const void* q_ptr;          // Q rows in global memory (TS kernel loads them into TMEM)
 };
 

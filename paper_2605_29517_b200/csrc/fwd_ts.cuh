@@ -349,7 +349,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kAtomBytes) >> 4);
         for (int mb = 0; mb < qbv; ++mb) {
           const int slot = mb & 1;
-          mbar_wait_idle(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
+          // profiling knob MXS_DEBUG=3 (bf16/fp16 only): never wait for the drain -- the raw
+          // MMA + TMA rate of this pipeline (accumulators overwritten, results garbage)
+          if (p.debug != 3) {
+            if (p.mma_spin)
+              mbar_wait(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
+            else
+              mbar_wait_idle(&hdr->tempty[slot], ((sbits >> slot) & 1u) ^ 1u);
+          }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
@@ -380,6 +387,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           phase ^= 1;
         }
       }
+    }
+    if (p.debug == 3) {  // nobody drained: wait for the last MMAs before TMEM is freed
+      if (elect_one()) mma_commit(&hdr->qempty);
+      __syncwarp();
+      mbar_wait(&hdr->qempty, qphase ^ 1u);
     }
   } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
@@ -432,6 +444,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         if (lane == 0) mbar_arrive(&hdr->qfull);
         cur_key = key;
       }
+      if (KIND != TcKind::I8 && p.debug == 3) continue;  // no drain (see the MMA issuer)
       const int vl = doc_valid_len(p, b);
       const int ntiles = (vl + kTileRows - 1) / kTileRows;
       float m[2], sq[2];

@@ -91,5 +91,8 @@ int main() {
   run<128, false>("SS  M128 N128 K16x8");
   run<256, false>("SS  M128 N256 K16x8");
   run<64, true>("TS  M128 N64  K16x8");
+  run<80, true>("TS  M128 N80  K16x8");
+  run<96, true>("TS  M128 N96  K16x8");
+  run<112, true>("TS  M128 N112 K16x8");
   return 0;
 }
