@@ -446,7 +446,12 @@ def run_e2e(a, Q, D, rank, world, dev, torch, dist):
         dq.copy_(hq, non_blocking=True)
         scores, ts, ti = mx.stream_score_host(dq[0], hd, k=a.topk, block_docs=1000)
         out_s[0].copy_(scores, non_blocking=True)
-        out_t.copy_(ti + rank * a.docs, non_blocking=True)
+        ti = ti + rank * a.docs
+        if world > 1:  # global top-K: the ranks' candidates, all-gathered and merged on the device
+            from paper_2605_29517_b200.topk import select_candidates
+
+            ts, ti = select_candidates(*_gather(ts.contiguous(), ti.contiguous(), world, dist), a.topk)
+        out_t.copy_(ti, non_blocking=True)
 
     one()
     torch.cuda.synchronize()
