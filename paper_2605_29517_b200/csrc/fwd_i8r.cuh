@@ -305,26 +305,36 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           tc_fence_after();
           uint32_t ra[32], rb[32];
           int cbd = 0;
-          tmem_ld32(taddr, ra);
-          tmem_ld32(taddr + 32, rb);
-          tmem_ld_wait();
           if (full) {
+            // software-pipelined drain: the TMEM load of chunk c + 1 is in flight while chunk c
+            // is folded (two 32-register buffers; the slot is released once chunk 3 has landed)
+            tmem_ld32(taddr, ra);
+            tmem_ld_wait_regs(ra);
+            tmem_ld32(taddr + 32, rb);
             ts_chunk_full<KIND, false, kI8>(ra, base, sqm, pm, cbd, nullptr, 0, sdt);
+            tmem_ld_wait_regs(rb);
+            tmem_ld32(taddr + 64, ra);
             ts_chunk_full<KIND, false, kI8>(rb, base + 32, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
-          } else {
-            ts_chunk<KIND, true, kI8>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
-            ts_chunk<KIND, true, kI8>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
-          }
-          tmem_ld32(taddr + 64, ra);
-          tmem_ld32(taddr + 96, rb);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&hdr->tempty[set]);
-          if (full) {
+            tmem_ld_wait_regs(ra);
+            tmem_ld32(taddr + 96, rb);
             ts_chunk_full<KIND, false, kI8>(ra, base + 64, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
+            tmem_ld_wait_regs(rb);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[set]);
             ts_chunk_full<KIND, false, kI8>(rb, base + 96, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           } else {
+            tmem_ld32(taddr, ra);
+            tmem_ld32(taddr + 32, rb);
+            tmem_ld_wait();
+            ts_chunk<KIND, true, kI8>(ra, base, vl, p, b, sqm, pm, cbd, nullptr, 0, sdt);
+            ts_chunk<KIND, true, kI8>(rb, base + 32, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 32 : nullptr);
+            tmem_ld32(taddr + 64, ra);
+            tmem_ld32(taddr + 96, rb);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[set]);
             ts_chunk<KIND, true, kI8>(ra, base + 64, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 64 : nullptr);
             ts_chunk<KIND, true, kI8>(rb, base + 96, vl, p, b, sqm, pm, cbd, nullptr, 0, kI8 ? sdt + 96 : nullptr);
           }
