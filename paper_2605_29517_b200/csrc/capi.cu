@@ -228,8 +228,9 @@ int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   p.argmax = nullptr;
   p.q_ptr = Q;
   {
-    const char* dbg = getenv("MXS_DEBUG");  // 3 (bf16/fp16): MMA never waits for the drain
-    p.debug = (dbg && !kI8) ? atoi(dbg) : 0;
+    const char* dbg = getenv("MXS_DEBUG");  // 2: slots released unread; 3 (bf16/fp16): no drain wait
+    p.debug = dbg ? atoi(dbg) : 0;
+    if (kI8 && p.debug == 3) p.debug = 0;
   }
   const CUtensorMapDataType dt = kI8                         ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : KIND == mxs::TcKind::BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16

@@ -305,7 +305,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           tc_fence_after();
           uint32_t ra[32], rb[32];
           int cbd = 0;
-          if (full) {
+          if (p.debug == 2) {  // profiling knob: release the slot unread (MMA + handshake bound)
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->tempty[set]);
+          } else if (full) {
             // software-pipelined drain: the TMEM load of chunk c + 1 is in flight while chunk c
             // is folded (two 32-register buffers; the slot is released once chunk 3 has landed)
             tmem_ld32(taddr, ra);
