@@ -8,7 +8,8 @@
 //
 // One CTA folds one (query, document) pair at a time: 32 query rows x 64 document tokens per
 // sub-tile, 8 accumulators per thread, the embedding axis streamed through shared memory in
-// chunks of 128 (the fold order over k is preserved across chunks).
+// chunks of 64 (the fold order over k is preserved across chunks).  Four k steps per LDS.128
+// (query row and the 8 broadcast document rows); one rounding per product and per add, in k order.
 #pragma once
 #include "ptx.cuh"
 #include <cuda_bf16.h>
@@ -25,6 +26,7 @@ struct FwdExactParams {
 };
 
 constexpr int kExRows = 32, kExCols = 64, kExK = 64, kExThreads = 256;
+constexpr int kExStride = kExK + 4;  // row pitch in floats: 16-B aligned rows, conflict-free LDS.128
 
 template <typename T>
 MXS_DEV float to_f32(T x);
@@ -35,17 +37,51 @@ MXS_DEV float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x
 template <>
 MXS_DEV float to_f32<__half>(__half x) { return __half2float(x); }
 
+// rows x kw elements of a row-major [*, dim] operand starting at (row0, k0) -> smem [rows][kExStride],
+// zero outside (rows_valid, kw).  fp32 with dim % 4 == 0: float4 loads.
+template <typename T, int ROWS>
+MXS_DEV void ex_stage(float (*dst)[kExStride], const T* src, int rows_valid, int dim, int k0, int kw, bool vec4) {
+  if constexpr (sizeof(T) == 4) {
+    if (vec4) {
+      for (int e = threadIdx.x; e < ROWS * (kExK / 4); e += kExThreads) {
+        const int rr = e / (kExK / 4), kk = (e % (kExK / 4)) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rr < rows_valid && kk < kw) v = __ldg(reinterpret_cast<const float4*>(src + (long long)rr * dim + k0 + kk));
+        *reinterpret_cast<float4*>(&dst[rr][kk]) = v;
+      }
+      return;
+    }
+  }
+  for (int e = threadIdx.x; e < ROWS * kExK; e += kExThreads) {
+    const int rr = e / kExK, kk = e % kExK;
+    dst[rr][kk] = (rr < rows_valid && kk < kw) ? to_f32(src[(long long)rr * dim + k0 + kk]) : 0.f;
+  }
+}
+
+// one k step of the sequential fold for the thread's 8 columns: __fmul_rn then __fadd_rn (scalar on
+// purpose -- ptxas contracts a packed mul.rn.f32x2 + add.rn.f32x2 pair into FFMA2, which would
+// round once instead of twice)
+template <bool kFirst>
+MXS_DEV void ex_step(float (&acc)[8], float qv, const float (&d)[8]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float t = __fmul_rn(qv, d[c]);
+    acc[c] = kFirst ? t : __fadd_rn(acc[c], t);
+  }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kExThreads) fwd_exact_kernel(const T* __restrict__ Q, const T* __restrict__ D,
+__global__ void __launch_bounds__(kExThreads, 3) fwd_exact_kernel(const T* __restrict__ Q, const T* __restrict__ D,
                                                                 const FwdExactParams p) {
-  __shared__ float sQ[kExRows][kExK + 1];
-  __shared__ float sD[kExCols][kExK + 1];
+  __shared__ __align__(16) float sQ[kExRows][kExStride];
+  __shared__ __align__(16) float sD[kExCols][kExStride];
   __shared__ float xm[8][kExRows];
   __shared__ int xi[8][kExRows];
   const int tid = threadIdx.x;
   const int i = tid & 31;   // query row within the row tile
   const int jg = tid >> 5;  // column phase: columns jg, jg+8, ...
   const long long n_pairs = (long long)p.n_q * p.n_docs;
+  const bool vec4 = sizeof(T) == 4 && (p.dim & 3) == 0;
   for (long long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
     const int q = (int)(pr / p.n_docs), b = (int)(pr % p.n_docs);
     long long drow0;
@@ -59,6 +95,7 @@ __global__ void __launch_bounds__(kExThreads) fwd_exact_kernel(const T* __restri
     }
     const T* qbase = Q + (long long)q * p.l_q * p.dim;
     const T* dbase = D + drow0 * p.dim;
+    const bool v4 = vec4 && ((reinterpret_cast<uintptr_t>(qbase) | reinterpret_cast<uintptr_t>(dbase)) & 15u) == 0;
     for (int r0 = 0; r0 < p.l_q; r0 += kExRows) {
       float m = -INFINITY;
       int ix = 0;
@@ -67,26 +104,37 @@ __global__ void __launch_bounds__(kExThreads) fwd_exact_kernel(const T* __restri
         for (int k0 = 0; k0 < p.dim; k0 += kExK) {
           const int kw = min(kExK, p.dim - k0);
           __syncthreads();
-          for (int e = tid; e < kExRows * kExK; e += kExThreads) {
-            const int rr = e / kExK, kk = e % kExK;
-            sQ[rr][kk] = (r0 + rr < p.l_q && kk < kw) ? to_f32(qbase[(long long)(r0 + rr) * p.dim + k0 + kk]) : 0.f;
-          }
-          for (int e = tid; e < kExCols * kExK; e += kExThreads) {
-            const int cc = e / kExK, kk = e % kExK;
-            sD[cc][kk] = (c0 + cc < vl && kk < kw) ? to_f32(dbase[(long long)(c0 + cc) * p.dim + k0 + kk]) : 0.f;
-          }
+          ex_stage<T, kExRows>(sQ, qbase + (long long)r0 * p.dim, p.l_q - r0, p.dim, k0, kw, v4);
+          ex_stage<T, kExCols>(sD, dbase + (long long)c0 * p.dim, vl - c0, p.dim, k0, kw, v4);
           __syncthreads();
-          int k = 0;
-          if (k0 == 0) {
-            const float qv = sQ[i][0];
+          const int kw4 = kw & ~3;
+          for (int k = 0; k < kw4; k += 4) {
+            const float4 qv = *reinterpret_cast<const float4*>(&sQ[i][k]);
+            float d0[8], d1[8], d2[8], d3[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[c] = __fmul_rn(qv, sD[jg + 8 * c][0]);
-            k = 1;
+            for (int c = 0; c < 8; ++c) {
+              const float4 dv = *reinterpret_cast<const float4*>(&sD[jg + 8 * c][k]);
+              d0[c] = dv.x;
+              d1[c] = dv.y;
+              d2[c] = dv.z;
+              d3[c] = dv.w;
+            }
+            if (k0 == 0 && k == 0)
+              ex_step<true>(acc, qv.x, d0);
+            else
+              ex_step<false>(acc, qv.x, d0);
+            ex_step<false>(acc, qv.y, d1);
+            ex_step<false>(acc, qv.z, d2);
+            ex_step<false>(acc, qv.w, d3);
           }
-          for (; k < kw; ++k) {
-            const float qv = sQ[i][k];
+          for (int k = kw4; k < kw; ++k) {  // dim % 4 tail
+            float dk[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(qv, sD[jg + 8 * c][k]));
+            for (int c = 0; c < 8; ++c) dk[c] = sD[jg + 8 * c][k];
+            if (k0 == 0 && k == 0)
+              ex_step<true>(acc, sQ[i][k], dk);
+            else
+              ex_step<false>(acc, sQ[i][k], dk);
           }
         }
 #pragma unroll
