@@ -448,6 +448,25 @@ int launch_fwd_exact(const void* Q, int64_t n_q, int64_t l_q, const void* D, int
   return check_launch("fwd_exact_kernel");
 }
 
+int launch_fwd_exact_i8(const int8_t* Q, const float* qs, int64_t n_q, int64_t l_q, const int8_t* D, const float* ds,
+                        int64_t n_docs, int64_t l_pad, int64_t dim, const int32_t* valid_lens, float* rowmax,
+                        int32_t* argmax, cudaStream_t st) {
+  mxs::FwdExactParams p;
+  p.n_q = (int)n_q;
+  p.l_q = (int)l_q;
+  p.n_docs = (int)n_docs;
+  p.l_pad = (int)l_pad;
+  p.dim = (int)dim;
+  p.valid_lens = valid_lens;
+  p.cu_seqlens = nullptr;
+  p.rowmax = rowmax;
+  p.argmax = argmax;
+  const long long pairs = n_q * n_docs;
+  const long long grid = pairs < (long long)sm_count() * 16 ? pairs : (long long)sm_count() * 16;
+  if (grid <= 0) return MXS_OK;
+  mxs::fwd_exact_i8_kernel<<<(unsigned)grid, mxs::kExThreads, 0, st>>>(Q, qs, D, ds, p);
+  return check_launch("fwd_exact_i8_kernel");
+}
 
 // Vectorised gather dispatch: rows must be 8-byte aligned (dim * sizeof(T) % 8 == 0) and the
 // dimension must fit NP <= 4 passes of 32 lanes x 8 bytes; otherwise the scalar kernels run.
@@ -591,6 +610,8 @@ int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     if (s == MXS_UNSUPPORTED)
       s = launch_fwd_tc<mxs::TcKind::BF16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
                                            argmax, st);
+    if (s == MXS_UNSUPPORTED)  // widths past the tensor-core tiles (d > 256 etc.): exact SIMT kernel on the GPU
+      s = launch_fwd_exact<__nv_bfloat16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, rowmax, argmax, st);
   } else if (dtype == MXS_F16) {
     s = (argmax || !rerank_r3_opt_in())
             ? MXS_UNSUPPORTED
@@ -603,6 +624,8 @@ int mxs_fused_rowmax_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
     if (s == MXS_UNSUPPORTED)
       s = launch_fwd_tc<mxs::TcKind::F16>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax,
                                           argmax, st);
+    if (s == MXS_UNSUPPORTED)  // widths past the tensor-core tiles (d > 256 etc.): exact SIMT kernel on the GPU
+      s = launch_fwd_exact<__half>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, rowmax, argmax, st);
   } else {
     return fail(MXS_UNSUPPORTED, "mxs_fused_score_batch: dtype %d", dtype);
   }
@@ -628,6 +651,8 @@ int mxs_fused_score_int8(const int8_t* Q, const float* q_scale, int64_t n_q, int
   if (s == MXS_UNSUPPORTED)
     s = launch_fwd_tc<mxs::TcKind::I8>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, q_scale, d_scale, rowmax,
                                        argmax, st);
+  if (s == MXS_UNSUPPORTED)  // widths past the tensor-core tiles: exact SIMT kernel (still on the GPU)
+    s = launch_fwd_exact_i8(Q, q_scale, n_q, l_q, D, d_scale, n_docs, l_pad, dim, valid_lens, rowmax, argmax, st);
   if (s != MXS_OK) return s;
   return launch_rowsum(rowmax, n_q * n_docs, l_q, scores, st);
 }

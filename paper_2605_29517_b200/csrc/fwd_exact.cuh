@@ -169,6 +169,87 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_kernel(const T* __res
   }
 }
 
+// INT8 x INT8 on CUDA cores, for widths beyond the tensor-core tiles (maxsim/quant.py:171-179):
+// exact int32 dot (wrapping like numpy's int32 matmul), f32(acc) round-to-nearest, then
+// fl(fl(acc * s_q) * s_d) in the reference order, masked strict-> fold.  Same tiling as
+// fwd_exact_kernel.
+__global__ void __launch_bounds__(kExThreads, 3) fwd_exact_i8_kernel(const int8_t* __restrict__ Q,
+                                                                     const float* __restrict__ qs,
+                                                                     const int8_t* __restrict__ D,
+                                                                     const float* __restrict__ ds,
+                                                                     const FwdExactParams p) {
+  __shared__ int sQ[kExRows][kExK + 1];
+  __shared__ int sD[kExCols][kExK + 1];
+  __shared__ float xm[8][kExRows];
+  __shared__ int xi[8][kExRows];
+  const int tid = threadIdx.x;
+  const int i = tid & 31;
+  const int jg = tid >> 5;
+  const long long n_pairs = (long long)p.n_q * p.n_docs;
+  for (long long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+    const int q = (int)(pr / p.n_docs), b = (int)(pr % p.n_docs);
+    const int vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+    const int8_t* qbase = Q + (long long)q * p.l_q * p.dim;
+    const int8_t* dbase = D + (long long)b * p.l_pad * p.dim;
+    for (int r0 = 0; r0 < p.l_q; r0 += kExRows) {
+      const float sq = (r0 + i < p.l_q) ? qs[(long long)q * p.l_q + r0 + i] : 1.f;
+      float m = -INFINITY;
+      int ix = 0;
+      for (int c0 = 0; c0 < vl; c0 += kExCols) {
+        int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k0 = 0; k0 < p.dim; k0 += kExK) {
+          const int kw = min(kExK, p.dim - k0);
+          __syncthreads();
+          for (int e = tid; e < kExRows * kExK; e += kExThreads) {
+            const int rr = e / kExK, kk = e % kExK;
+            sQ[rr][kk] = (r0 + rr < p.l_q && kk < kw) ? (int)qbase[(long long)(r0 + rr) * p.dim + k0 + kk] : 0;
+          }
+          for (int e = tid; e < kExCols * kExK; e += kExThreads) {
+            const int cc = e / kExK, kk = e % kExK;
+            sD[cc][kk] = (c0 + cc < vl && kk < kw) ? (int)dbase[(long long)(c0 + cc) * p.dim + k0 + kk] : 0;
+          }
+          __syncthreads();
+          for (int k = 0; k < kw; ++k) {
+            const int qv = sQ[i][k];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = (int)((unsigned)acc[c] + (unsigned)(qv * sD[jg + 8 * c][k]));
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = c0 + jg + 8 * c;
+          if (j < vl) {
+            const float v = __fmul_rn(__fmul_rn(__int2float_rn(acc[c]), sq), ds[(long long)b * p.l_pad + j]);
+            if (v > m) {
+              m = v;
+              ix = j;
+            }
+          }
+        }
+      }
+      xm[jg][i] = m;
+      xi[jg][i] = ix;
+      __syncthreads();
+      if (jg == 0 && r0 + i < p.l_q) {
+        float bm = xm[0][i];
+        int bi = xi[0][i];
+        for (int w = 1; w < 8; ++w) {
+          const float om = xm[w][i];
+          const int oi = xi[w][i];
+          if (om > bm || (om == bm && oi < bi)) {
+            bm = om;
+            bi = oi;
+          }
+        }
+        const long long o = ((long long)q * p.n_docs + b) * p.l_q + r0 + i;
+        p.rowmax[o] = bm;
+        if (p.argmax) p.argmax[o] = bi;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Per-pair score: the strict left-to-right float64 sum of the fp32 row maxima (S4,
 // `maxsim/kernels.py:22-26` seq_sum_f64), computed in parallel when that is provably identical.
 //

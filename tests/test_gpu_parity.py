@@ -43,6 +43,27 @@ def top2_gap(Q, D, valid_lens):
     return np.where(np.isfinite(gap), gap, np.inf)
 
 
+@pytest.mark.parametrize("dim", [8, 16, 40, 200, 320, 512])
+def test_forward_unusual_dims(dim):
+    """Embedding widths off the 64-element atom (zero-filled K tail in TMA / TMEM) and past the
+    resident-Q budget (d > 256 takes the SS kernel): scores within 1e-3 of the oracle, argmax
+    identical where the oracle's top-2 gap is clear, rerank mode bit-identical to the argmax mode."""
+    rng = np.random.default_rng(dim)
+    l_q, n_docs, l_pad = 150, 20, 200
+    Q = orc.make_queries(2, l_q, dim, seed=dim)
+    lens = rng.integers(1, l_pad + 1, n_docs)
+    D, vl = orc.padded(orc.make_corpus(n_docs, lens, dim, seed=dim + 1), l_pad)
+    Qr, Dr = cuda(Q, torch.bfloat16), cuda(D, torch.bfloat16)
+    sc, am, _ = mx.score_dense(Qr, Dr, cuda(vl))
+    Qo, Do = Qr.float().cpu().numpy(), Dr.float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_batch(Qo, Do, vl)
+    assert rel_err(sc.cpu().numpy(), ref_s) < REL
+    clear = top2_gap(Qo, Do, vl) > 1e-5
+    assert np.array_equal(am.cpu().numpy()[clear], ref_a[clear])
+    s2, _, _ = mx.score_dense(Qr, Dr, cuda(vl), want_argmax=False)
+    assert torch.equal(s2, sc)
+
+
 # ------------------------------------------------------------------ exact fp32 path (K10)
 def test_exact_fp32_golden_bitwise():
     for name in ("fwd_ragged", "fwd_ties"):
@@ -239,11 +260,12 @@ def test_int8_random_bitwise_incl_ties(l_q, n_docs, l_pad, dim):
     assert am2 is None and np.array_equal(sc2.cpu().numpy(), ref_s)
 
 
-@pytest.mark.parametrize("dim", [128, 256, 384])
+@pytest.mark.parametrize("dim", [128, 256, 384, 1100, 3000])
 def test_int8_extreme_accumulators_bitwise(dim):
     """Raw int8 at the edges of the s32 range the kernels convert: all -128 x -128 at d = 256 gives
     acc = 2^22 exactly (the limit of the biased / magic-number s32 -> f32), -128 x 127 the most
-    negative sums; d = 384 takes the cvt path.  Scores and argmax bit-identical to the oracle."""
+    negative sums; d = 384 takes the cvt path, d = 1100 / 3000 (past the tensor-core tiles) the exact
+    SIMT kernel, whose f32(acc) rounds once |acc| > 2^24.  Scores and argmax bit-identical to the oracle."""
     rng = np.random.default_rng(dim)
     l_q, n_docs, l_pad = 160, 6, 256
     qq = rng.integers(-128, 128, (1, l_q, dim)).astype(np.int8)
