@@ -714,6 +714,8 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
     cudaFuncSetAttribute(mxs::csr_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(mxs::csr_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(mxs::csr_place_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mxs::csr_count_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(mxs::csr_place_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   });
   const unsigned segs = (unsigned)(n_q * n_docs);
   // rows that belong to no document (never the case for padded / packed layouts) stay zero
@@ -721,12 +723,21 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
     return fail(MXS_CUDA_ERROR, "memset");
   if (cudaMemsetAsync(row_ptr, 0, sizeof(int32_t) * (size_t)(n_dest + 1), st) != cudaSuccess)
     return fail(MXS_CUDA_ERROR, "memset");
-  mxs::csr_count_kernel<<<segs, 256, hist_bytes, st>>>(p);
   int s;
+  const bool warp_seg = max_dest_len <= mxs::kCsrWarpLenMax && !getenv("MXS_CSR_BLOCK");
+  const int hist_len = (int)((max_dest_len + 3) & ~3LL);
+  const size_t wsh = (size_t)mxs::kCsrWW * hist_len * sizeof(int32_t);
+  const unsigned wblocks = (unsigned)((segs + mxs::kCsrWW - 1) / mxs::kCsrWW);
+  if (warp_seg)
+    mxs::csr_count_w_kernel<<<wblocks, 32 * mxs::kCsrWW, wsh, st>>>(p, hist_len);
+  else
+    mxs::csr_count_kernel<<<segs, 256, hist_bytes, st>>>(p);
   if ((s = check_launch("csr_count_kernel")) != MXS_OK) return s;
   mxs::csr_scan_kernel<<<(unsigned)n_docs, 1024, 0, st>>>(p);
   if ((s = check_launch("csr_scan_kernel")) != MXS_OK) return s;
-  if (hist_bytes * mxs::kCsrWarps <= 200 * 1024)
+  if (warp_seg)
+    mxs::csr_place_w_kernel<<<wblocks, 32 * mxs::kCsrWW, wsh, st>>>(p, hist_len);
+  else if (hist_bytes * mxs::kCsrWarps <= 200 * 1024)
     mxs::csr_place_v2_kernel<<<segs, 32 * mxs::kCsrWarps, hist_bytes * mxs::kCsrWarps, st>>>(p);
   else
     mxs::csr_place_kernel<<<segs, 256, hist_bytes, st>>>(p);

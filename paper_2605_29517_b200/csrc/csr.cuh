@@ -58,8 +58,10 @@ __global__ void __launch_bounds__(1024) csr_scan_kernel(const CsrParams p) {
   for (int t0 = 0; t0 < len; t0 += blockDim.x) {
     const int t = t0 + threadIdx.x;
     int tot = 0;
-    if (t < len)
-      for (int q = 0; q < p.n_q; ++q) tot += p.cnt[(long long)q * p.n_dest + off + t];
+    if (t < len) {
+#pragma unroll 16
+      for (int q = 0; q < p.n_q; ++q) tot += p.cnt[(long long)q * p.n_dest + off + t];  // 16 loads in flight
+    }
     // block exclusive scan of tot
     int x = tot;
 #pragma unroll
@@ -83,7 +85,18 @@ __global__ void __launch_bounds__(1024) csr_scan_kernel(const CsrParams p) {
     if (t < len) {
       p.row_ptr[off + t] = excl;
       int run = excl;
-      for (int q = 0; q < p.n_q; ++q) {
+      int q0 = 0;
+      for (; q0 + 16 <= p.n_q; q0 += 16) {  // 16 independent loads, then the running prefix
+        int v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = p.cnt[(long long)(q0 + u) * p.n_dest + off + t];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          p.cnt[(long long)(q0 + u) * p.n_dest + off + t] = run;
+          run += v[u];
+        }
+      }
+      for (int q = q0; q < p.n_q; ++q) {
         int32_t* c = p.cnt + (long long)q * p.n_dest + off + t;
         const int v = *c;
         *c = run;
@@ -175,6 +188,80 @@ __global__ void __launch_bounds__(32 * kCsrWarps) csr_place_v2_kernel(const CsrP
     __syncwarp();
     if (ok && rank == 0) h[key] += __popc(peers);
     __syncwarp();
+  }
+}
+
+// Warp-per-segment variants (used when every document has at most kCsrWarpLenMax rows): a
+// block holds kCsrWW segments, each warp its own shared-memory histogram / cursor array, so a
+// (q, b) segment needs no block barrier and all 4096 segments of C3 are resident in one wave
+// (the block-per-segment kernels above ran ~4 waves of tiny blocks).
+constexpr int kCsrWW = 8;
+constexpr int kCsrWarpLenMax = 1536;  // 8 warps x 1536 x 4 B = 48 KB per block
+
+__global__ void __launch_bounds__(32 * kCsrWW) csr_count_w_kernel(const CsrParams p, int hist_len) {
+  extern __shared__ int32_t csr_sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long seg = (long long)blockIdx.x * kCsrWW + w;
+  if (seg >= (long long)p.n_q * p.n_docs) return;  // warp-uniform; no block barrier below
+  const int q = (int)(seg / p.n_docs), b = (int)(seg % p.n_docs);
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  int32_t* hist = csr_sh + w * hist_len;
+  for (int t = lane; t < len; t += 32) hist[t] = 0;
+  __syncwarp();
+  const int32_t* a = p.argmax + seg * p.l_q;
+  for (int i = lane; i < p.l_q; i += 32) {
+    const int key = __ldg(a + i);
+    if (key >= 0 && key < len) atomicAdd(&hist[key], 1);
+  }
+  __syncwarp();
+  int32_t* out = p.cnt + (long long)q * p.n_dest + off;
+  for (int t = lane; t < len; t += 32) out[t] = hist[t];
+}
+
+// Stable placement, one warp per (q, b) segment: 32 sources per step in source order; ranks of
+// equal keys inside the step from __match_any_sync, the bucket cursor advanced by the lowest lane
+// of each key group after everyone has read it.  Keys are prefetched 8 steps at a time.
+__global__ void __launch_bounds__(32 * kCsrWW) csr_place_w_kernel(const CsrParams p, int hist_len) {
+  extern __shared__ int32_t csr_sh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long seg = (long long)blockIdx.x * kCsrWW + w;
+  if (seg >= (long long)p.n_q * p.n_docs) return;
+  const int q = (int)(seg / p.n_docs), b = (int)(seg % p.n_docs);
+  const long long off = p.dest_off[b];
+  const int len = (int)p.dest_len[b];
+  int32_t* cursor = csr_sh + w * hist_len;
+  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;  // first slot of (q, b) per bucket
+  for (int t = lane; t < len; t += 32) cursor[t] = base[t];
+  __syncwarp();
+  const long long src0 = seg * p.l_q;
+  const int32_t* a = p.argmax + src0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int e0 = 0; e0 < p.l_q; e0 += 32 * 8) {
+    int keys[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = e0 + 32 * u + lane;
+      keys[u] = i < p.l_q ? __ldg(a + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = e0 + 32 * u + lane;
+      if (e0 + 32 * u >= p.l_q) break;  // warp-uniform
+      int key = keys[u];
+      const bool ok = i < p.l_q && key >= 0 && key < len;
+      if (!ok) key = -1 - lane;  // distinct dummy keys never match real ones
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int rank = __popc(peers & lt_mask);
+      int slot = 0;
+      if (ok) slot = cursor[key] + rank;
+      __syncwarp();
+      if (ok) {
+        p.col_idx[slot] = (int32_t)(src0 + i);
+        if (rank == 0) cursor[key] += __popc(peers);
+      }
+      __syncwarp();
+    }
   }
 }
 
