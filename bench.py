@@ -494,8 +494,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        # test knob: every rank on cuda:0 over gloo, to exercise the N > 1 code path on a 1-GPU box
+        one_gpu = os.environ.get("MXS_BENCH_ONE_GPU") == "1"
+        if one_gpu:
+            local_rank = 0
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(a, rank, world, local_rank)
     finally:
