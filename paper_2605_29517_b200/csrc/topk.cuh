@@ -162,9 +162,10 @@ MXS_DEV bool sel_before(double s1, long long i1, double s2, long long i2) {
 
 constexpr int kSelSurvivors = 1024;  // threshold-filter capacity (one sort element per thread pair)
 
-// Threshold filter for k <= 32.  Every lane's maximum is a real element, so the k-th largest lane
-// maximum of ANY warp is a lower bound T on the k-th largest score of the slice; the largest
-// such bound over the warps is used.  Only elements with score >= T can be in the top k; they
+// Threshold filter for k <= kSelMaxK.  Every lane's maximum is a real element, so for k <= 32 the
+// k-th largest lane maximum of ANY warp is a lower bound T on the k-th largest score of the slice
+// (the largest such bound over the warps is used); for larger k, the k-th largest of all the
+// block's lane maxima.  Only elements with score >= T can be in the top k; they
 // are compacted (typically k .. a few k of them) and sorted with a bitonic network under the
 // reference order.  Returns false (nothing written) if more than kSelSurvivors survive -- e.g.
 // massive ties at the threshold -- and the caller falls back to the warp tournaments.
@@ -178,25 +179,50 @@ MXS_DEV bool sel_threshold(const double* ss, const long long* si, long long base
   // 1. lane maxima (NaN = empty never wins: the comparison is false)
   double lm = -INFINITY;
   for (int j = b0 + lane; j < b1; j += 32) lm = fmax(lm, ss[j]);
-  // 2. k-th largest lane maximum of this warp: bitonic sort of 32 values (descending)
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, lm, stride);
-      const bool lower = (lane & stride) == 0;
-      const bool desc = (lane & size) == 0 || size == 32;
-      // in a descending run the lower lane keeps the max
-      lm = (lower == desc) ? fmax(lm, o) : fmin(lm, o);
-    }
-  }
-  const double kth = __shfl_sync(0xffffffffu, lm, k - 1);
-  if (lane == 0) wbound[w] = kth;
-  if (threadIdx.x == 0) *counter = 0;
-  __syncthreads();
   double T = -INFINITY;
+  if (k <= 32) {
+    // 2. k-th largest lane maximum of this warp: bitonic sort of 32 values (descending)
 #pragma unroll
-  for (int i = 0; i < kWarps; ++i) T = fmax(T, wbound[i]);
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, lm, stride);
+        const bool lower = (lane & stride) == 0;
+        const bool desc = (lane & size) == 0 || size == 32;
+        // in a descending run the lower lane keeps the max
+        lm = (lower == desc) ? fmax(lm, o) : fmin(lm, o);
+      }
+    }
+    const double kth = __shfl_sync(0xffffffffu, lm, k - 1);
+    if (lane == 0) wbound[w] = kth;
+    if (threadIdx.x == 0) *counter = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) T = fmax(T, wbound[i]);
+  } else {
+    // 2'. k in (32, kSelThreads]: the k-th largest of ALL the block's lane maxima (distinct real
+    //     elements, so again a lower bound), by a bitonic sort of the kSelThreads lane maxima
+    sv_s[threadIdx.x] = lm;
+    if (threadIdx.x == 0) *counter = 0;
+    __syncthreads();
+    for (int size = 2; size <= kSelThreads; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < kSelThreads / 2; t += blockDim.x) {
+          const int a = 2 * t - (t & (stride - 1));
+          const int b = a + stride;
+          const bool desc = (a & size) == 0 || size == kSelThreads;
+          const double va = sv_s[a], vb = sv_s[b];
+          if ((vb > va) == desc) {
+            sv_s[a] = vb;
+            sv_s[b] = va;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    T = sv_s[k - 1];
+    __syncthreads();  // sv_s is reused for the survivors below
+  }
   // 3. compact the survivors (score >= T); with T = -inf (fewer than k valid entries in every
   //    warp) everything valid survives and the capacity check decides
   for (int j = b0 + lane; j < b1; j += 32) {
@@ -280,7 +306,7 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* 
   __syncthreads();
   double* os = out_s + (long long)blockIdx.x * k;
   long long* oi = out_ids + (long long)blockIdx.x * k;
-  if (k <= 32 && sel_threshold(ss, si, lo + id_offset, m, k, os, oi, sv_s, sv_i, wbound, &counter)) return;
+  if (k <= kSelMaxK && sel_threshold(ss, si, lo + id_offset, m, k, os, oi, sv_s, sv_i, wbound, &counter)) return;
   const int w = (int)warp_id_uniform();
   const int per = (m + kWarps - 1) / kWarps;
   const int b0 = min(m, w * per), b1 = min(m, b0 + per);

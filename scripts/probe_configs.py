@@ -67,6 +67,14 @@ peak8 = 2 * 8192 ** 3 / t_mm / 1e9
 print(f"C4 roofline: int8 peak (torch._int_mm 8192^3) {peak8:.0f} TOP/s; rerank kernel {2.684e12 / t_i8 / 1e9:.0f} TOP/s "
       f"= {2.684e12 / t_i8 / 1e9 / peak8:.1%} of measured, {2.684e12 / t_i8 / 1e9 / 4500:.1%} of 4.5 POPS spec")
 del a8, b8
+# two-stage top-20 (INT8 scan of all 10K docs, bf16 rescoring of the 80-doc shortlist), public API
+corpus_q = mx.QuantizedCorpus(dq, ds) if hasattr(mx, "QuantizedCorpus") else None
+full = mx.DocBatch.from_dense(Df)
+try:
+    t_2s = timeit(lambda: mx.two_stage_topk(Qf[0], corpus_q, full, k=20), reps=5, warm=2)
+    print(f"C4 two-stage top-20 of {nb}: {t_2s:.3f} ms ({nb / t_2s * 1e3 / 1e6:.2f} M docs/s) incl. host result list")
+except Exception as e:  # report, do not abort the probe
+    print(f"C4 two-stage: {type(e).__name__}: {e}")
 del Df, dq
 
 # C5 scaled: varlen 100K docs L in [32, 512], L_q = 32
