@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -259,6 +260,27 @@ def stream_score_topk(query, corpus, block_docs: int, k: int, tile: TileConfig =
             own.close()
 
 
+# Staging buffers (2 pinned host + 2 device) reused across stream_score_topk calls: allocating
+# ~GB of pinned memory per call costs more than streaming a small corpus.  One cached set per
+# (device, size); a call that finds it in use (concurrent callers) allocates its own.
+_STAGING: dict = {}
+_STAGING_LOCK = threading.Lock()
+
+
+def _staging(dev, cap):
+    key = (str(dev), int(cap))
+    if _STAGING_LOCK.acquire(blocking=False):
+        bufs = _STAGING.get(key)
+        if bufs is None:
+            _STAGING.clear()
+            bufs = ([torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+                    [torch.empty(cap, dtype=torch.uint8, device=dev) for _ in range(2)])
+            _STAGING[key] = bufs
+        return bufs, _STAGING_LOCK.release
+    return ([torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+            [torch.empty(cap, dtype=torch.uint8, device=dev) for _ in range(2)]), (lambda: None)
+
+
 def _stream(query, reader: CorpusReader, block_docs: int, k: int, report, compute_dtype):
     from .varlen import score_varlen
     from .forward import score_dense
@@ -287,8 +309,7 @@ def _stream(query, reader: CorpusReader, block_docs: int, k: int, report, comput
     q = q.to(work_dtype).contiguous()
     blocks = [(f, min(block_docs, n_docs - f)) for f in range(0, n_docs, block_docs)]
     cap = max(reader.block_bytes(f, c) for f, c in blocks)
-    host = [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-    devb = [torch.empty(cap, dtype=torch.uint8, device=dev) for _ in range(2)]
+    (host, devb), release_staging = _staging(dev, cap)
     h2d_done = [None, None]
     dev_free = [None, None]
     copy_stream = torch.cuda.Stream(device=dev)
@@ -349,6 +370,8 @@ def _stream(query, reader: CorpusReader, block_docs: int, k: int, report, comput
         return [(int(a), float(b)) for a, b in zip(ids, vals)][:k], rep
     finally:
         pool.shutdown(wait=True)
+        torch.cuda.current_stream(dev).synchronize()  # staging buffers are idle before reuse
+        release_staging()
 
 
 def stream_score_host(query, docs_host: torch.Tensor, k: int, block_docs: int = 1000, valid_lens=None,
