@@ -53,8 +53,10 @@ inline int64_t pread_all(int fd, void* dst, int64_t n, int64_t off) {
 
 // Large ranges are split over a few threads (page cache / NVMe parallelism).
 inline int64_t pread_parallel(int fd, void* dst, int64_t n, int64_t off) {
-  constexpr int64_t kPiece = 64ll << 20;
-  const int nt = (int)std::min<int64_t>(8, (n + kPiece - 1) / kPiece);
+  constexpr int64_t kPiece = 32ll << 20;
+  // page-cache -> pinned copies are host-memory-bandwidth bound: use up to 16 cores
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(std::min<int64_t>(16, hw), (n + kPiece - 1) / kPiece);
   if (nt <= 1) return pread_all(fd, dst, n, off);
   std::vector<std::thread> th;
   std::vector<int64_t> got(nt, 0);
