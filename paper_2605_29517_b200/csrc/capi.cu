@@ -668,7 +668,17 @@ int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, 
   const long long blocks = (rows * 32 + 255) / 256;
   if (dtype == MXS_F32)
     mxs::quantize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x, rows, (int)dim, levels, q, scale);
-  else if (dtype == MXS_BF16 && dim == 128)
+  else if ((dtype == MXS_BF16 || dtype == MXS_F16) && dim == 128 &&
+           (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+    // persistent 8-lanes-per-row kernel: 8 blocks of 256 threads per SM
+    const long long want = (rows + 63) / 64;  // 32 groups x 2 rows per block pass (U = 4: 93 regs, slower)
+    const long long sblocks = want < (long long)sm_count() * 8 ? want : (long long)sm_count() * 8;
+    if (dtype == MXS_BF16)
+      mxs::quantize128_stream_kernel<__nv_bfloat16, 2>
+          <<<(unsigned)sblocks, 256, 0, st>>>((const __nv_bfloat16*)x, rows, levels, q, scale);
+    else
+      mxs::quantize128_stream_kernel<__half, 2><<<(unsigned)sblocks, 256, 0, st>>>((const __half*)x, rows, levels, q, scale);
+  } else if (dtype == MXS_BF16 && dim == 128)
     mxs::quantize128_kernel<__nv_bfloat16>
         <<<(unsigned)blocks, 256, 0, st>>>((const __nv_bfloat16*)x, rows, levels, q, scale);
   else if (dtype == MXS_F16 && dim == 128)

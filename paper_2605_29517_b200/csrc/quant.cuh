@@ -74,4 +74,74 @@ __global__ void __launch_bounds__(256) quantize128_kernel(const T* __restrict__ 
   reinterpret_cast<uint32_t*>(q + warp * 128)[lane] = packed;
 }
 
+
+// Streaming variant for bf16 / f16 rows with dim == 128 (the C4 corpus, HBM-bound): 8 lanes own
+// a row (32 B = 16 elements each, so the per-row reduction / division / reciprocal is amortised
+// over 16 elements per lane), each 8-lane group keeps two rows in flight, and the grid is
+// persistent (grid-stride), so one row's arithmetic overlaps the next rows' loads.  Same
+// arithmetic as quantize128_kernel (bit-exact); the rounding check is on the distance to the
+// nearest integer (|y - rint(y)| near 1/2 <=> y near a half-integer).
+MXS_DEV float quant_round_fast(float x, float s, float r) {
+  const float y = __fmul_rn(x, r);
+  const float t = rintf(y);
+  if (fabsf(y - t) > 0.5f - 0x1p-12f) return rintf(__fdiv_rn(x, s));
+  return t;
+}
+
+template <typename T, int U>
+__global__ void __launch_bounds__(256) quantize128_stream_kernel(const T* __restrict__ x, long long rows, int levels,
+                                                                 int8_t* __restrict__ q, float* __restrict__ scale) {
+  static_assert(sizeof(T) == 2, "16-bit rows");
+  const int l8 = threadIdx.x & 7;
+  const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;  // 8-lane group id
+  const long long n_grp = ((long long)gridDim.x * blockDim.x) >> 3;
+  const float lv = (float)levels;
+  for (long long r0 = grp; r0 - grp < rows; r0 += U * n_grp) {  // warp-uniform trip count
+    long long row[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) row[u] = r0 + u * n_grp;
+    uint4 raw[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      raw[u][0] = raw[u][1] = make_uint4(0u, 0u, 0u, 0u);
+      if (row[u] < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + row[u] * 128) + 2 * l8;
+        raw[u][0] = __ldg(src);
+        raw[u][1] = __ldg(src + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float v[16];
+      const T* h = reinterpret_cast<const T*>(&raw[u][0]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = to_f32(h[j]);
+      float mx = fabsf(v[0]);
+#pragma unroll
+      for (int j = 1; j < 16; ++j) mx = fmaxf(mx, fabsf(v[j]));
+#pragma unroll
+      for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));  // within the 8 lanes
+      if (row[u] < rows) {
+        float s = __fdiv_rn(mx, lv);
+        if (s == 0.f) s = 1e-12f;
+        if (l8 == 0) scale[row[u]] = s;
+        const float r = __frcp_rn(s);
+        // no clamp needed here: |x| <= maxabs and s = fl(maxabs / levels) give |x / s| <= levels
+        // (1 + 2^-23), and x * fl(1 / s) adds two more ulps -- far below the 0.5 that rint would
+        // need to reach levels + 1 (zero rows: x = 0).  The reference's clip is a no-op on them.
+        uint32_t w[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          int t[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) t[j] = (int)quant_round_fast(v[4 * c + j], s, r);
+          w[c] = __byte_perm(__byte_perm((uint32_t)t[0], (uint32_t)t[1], 0x0040), __byte_perm((uint32_t)t[2], (uint32_t)t[3], 0x0040),
+                             0x5410);
+        }
+        reinterpret_cast<uint4*>(q + row[u] * 128)[l8] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
+
 }  // namespace mxs
