@@ -6,6 +6,7 @@
 #include <cstring>
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 #include <string>
 
 #include "../../include/maxsim_b200.h"
@@ -443,6 +444,20 @@ int launch_fwd_exact(const void* Q, int64_t n_q, int64_t l_q, const void* D, int
   const int nsm = sm_count();
   long long grid = pairs < (long long)nsm * 16 ? pairs : (long long)nsm * 16;
   if (grid <= 0) return MXS_OK;
+  if constexpr (std::is_same<T, float>::value) {
+    // double-buffered cp.async variant: 16-B aligned rows (dim % 4 == 0, aligned bases)
+    if (dim % 4 == 0 && ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(D)) & 15) == 0 &&
+        !getenv("MXS_EXACT_V1")) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(mxs::fwd_exact_f32v_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mxs::kExV4Smem);
+      });
+      mxs::fwd_exact_f32v_kernel<<<(unsigned)grid, mxs::kExThreads, mxs::kExV4Smem, st>>>(
+          static_cast<const float*>(Q), static_cast<const float*>(D), p);
+      return check_launch("fwd_exact_f32v_kernel");
+    }
+  }
   mxs::fwd_exact_kernel<T><<<(unsigned)grid, mxs::kExThreads, 0, st>>>(static_cast<const T*>(Q),
                                                                         static_cast<const T*>(D), p);
   return check_launch("fwd_exact_kernel");

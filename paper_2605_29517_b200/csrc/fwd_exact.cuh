@@ -169,6 +169,133 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_kernel(const T* __res
   }
 }
 
+// fp32 rows, dim % 4 == 0, 16-B aligned: the same fold with the (column tile, k chunk) stages
+// double-buffered through cp.async (16-B LDGSTS, zero-fill outside the valid rows / width), so
+// stage s + 1 streams in while stage s is folded.  Dynamic smem: 2 x (32 + 64) rows x 68 floats.
+MXS_DEV void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+MXS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MXS_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr size_t kExV4Smem = (size_t)2 * (kExRows + kExCols) * kExStride * sizeof(float);
+
+__global__ void __launch_bounds__(kExThreads, 3) fwd_exact_f32v_kernel(const float* __restrict__ Q,
+                                                                       const float* __restrict__ D,
+                                                                       const FwdExactParams p) {
+  extern __shared__ __align__(16) float ex_smem[];
+  float(*sQ)[kExRows][kExStride] = reinterpret_cast<float(*)[kExRows][kExStride]>(ex_smem);
+  float(*sD)[kExCols][kExStride] = reinterpret_cast<float(*)[kExCols][kExStride]>(ex_smem + 2 * kExRows * kExStride);
+  __shared__ float xm[8][kExRows];
+  __shared__ int xi[8][kExRows];
+  const int tid = threadIdx.x;
+  const int i = tid & 31;
+  const int jg = tid >> 5;
+  const long long n_pairs = (long long)p.n_q * p.n_docs;
+  const int nk = (p.dim + kExK - 1) / kExK;
+  for (long long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+    const int q = (int)(pr / p.n_docs), b = (int)(pr % p.n_docs);
+    long long drow0;
+    int vl;
+    if (p.cu_seqlens) {
+      drow0 = p.cu_seqlens[b];
+      vl = (int)(p.cu_seqlens[b + 1] - drow0);
+    } else {
+      drow0 = (long long)b * p.l_pad;
+      vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+    }
+    const float* qbase = Q + (long long)q * p.l_q * p.dim;
+    const float* dbase = D + drow0 * p.dim;
+    const int nc = (vl + kExCols - 1) / kExCols;
+    for (int r0 = 0; r0 < p.l_q; r0 += kExRows) {
+      auto issue = [&](int st, int buf) {
+        const int c0 = (st / nk) * kExCols, k0 = (st % nk) * kExK;
+        const int kw = min(kExK, p.dim - k0);
+        for (int e = tid; e < kExRows * (kExK / 4); e += kExThreads) {
+          const int rr = e / (kExK / 4), kk = (e % (kExK / 4)) * 4;
+          const bool ok = r0 + rr < p.l_q && kk < kw;
+          cp_async16(&sQ[buf][rr][kk], ok ? qbase + (long long)(r0 + rr) * p.dim + k0 + kk : qbase, ok);
+        }
+        for (int e = tid; e < kExCols * (kExK / 4); e += kExThreads) {
+          const int cc = e / (kExK / 4), kk = (e % (kExK / 4)) * 4;
+          const bool ok = c0 + cc < vl && kk < kw;
+          cp_async16(&sD[buf][cc][kk], ok ? dbase + (long long)(c0 + cc) * p.dim + k0 + kk : dbase, ok);
+        }
+        cp_async_commit();
+      };
+      float m = -INFINITY;
+      int ix = 0;
+      float acc[8];
+      const int nst = nc * nk;
+      if (nst > 0) issue(0, 0);
+      for (int st = 0; st < nst; ++st) {
+        const int buf = st & 1;
+        if (st + 1 < nst) {
+          issue(st + 1, buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int c0 = (st / nk) * kExCols, k0 = (st % nk) * kExK;
+        const int kw = min(kExK, p.dim - k0);
+        for (int k = 0; k < kw; k += 4) {
+          const float4 qv = *reinterpret_cast<const float4*>(&sQ[buf][i][k]);
+          float d0[8], d1[8], d2[8], d3[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 dv = *reinterpret_cast<const float4*>(&sD[buf][jg + 8 * c][k]);
+            d0[c] = dv.x;
+            d1[c] = dv.y;
+            d2[c] = dv.z;
+            d3[c] = dv.w;
+          }
+          if (k0 == 0 && k == 0)
+            ex_step<true>(acc, qv.x, d0);
+          else
+            ex_step<false>(acc, qv.x, d0);
+          ex_step<false>(acc, qv.y, d1);
+          ex_step<false>(acc, qv.z, d2);
+          ex_step<false>(acc, qv.w, d3);
+        }
+        if (st % nk == nk - 1) {  // column tile complete: fold in column order
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int j = c0 + jg + 8 * c;
+            if (j < vl && acc[c] > m) {
+              m = acc[c];
+              ix = j;
+            }
+          }
+        }
+        __syncthreads();  // buffer `buf` is refilled by the issue of stage st + 2
+      }
+      xm[jg][i] = m;
+      xi[jg][i] = ix;
+      __syncthreads();
+      if (jg == 0 && r0 + i < p.l_q) {
+        float bm = xm[0][i];
+        int bi = xi[0][i];
+        for (int w = 1; w < 8; ++w) {
+          const float om = xm[w][i];
+          const int oi = xi[w][i];
+          if (om > bm || (om == bm && oi < bi)) {
+            bm = om;
+            bi = oi;
+          }
+        }
+        const long long o = ((long long)q * p.n_docs + b) * p.l_q + r0 + i;
+        p.rowmax[o] = bm;
+        if (p.argmax) p.argmax[o] = bi;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // INT8 x INT8 on CUDA cores, for widths beyond the tensor-core tiles (maxsim/quant.py:171-179):
 // exact int32 dot (wrapping like numpy's int32 matmul), f32(acc) round-to-nearest, then
 // fl(fl(acc * s_q) * s_d) in the reference order, masked strict-> fold.  Same tiling as
