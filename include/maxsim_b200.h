@@ -3,8 +3,8 @@
  *
  * Conventions (all entry points):
  *   - every pointer argument is a DEVICE pointer unless stated otherwise; the caller owns
- *     every buffer (no allocation happens inside the library except cached TMA descriptors
- *     on the host stack);
+ *     every output buffer (the only internal allocation is a stream-ordered cudaMallocAsync
+ *     row-maxima scratch when a forward needs a separate S4 pass and rowmax is NULL);
  *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered and returns
  *     as soon as the work is enqueued;
  *   - the return value is an mxs_status; MXS_OK == 0.  mxs_last_error() returns a
@@ -46,6 +46,19 @@ typedef enum {
 
 typedef enum { MXS_F32 = 0, MXS_F16 = 1, MXS_BF16 = 2, MXS_I8 = 3 } mxs_dtype;
 
+/*
+ * Input validation that needs the data (synchronous on `stream`: one small kernel + a 16-byte
+ * read-back).  Replaces the checks of maxsim/forward.py:173-176 / maxsim/types.py:97-98
+ * (valid_len < 1 -> EmptyDocument(index), valid_len > rows -> ShapeMismatch) and
+ * maxsim/varlen.py:35-41 (cu[0] != 0 or cu[B] != n_tokens -> ShapeMismatch, a non-increasing
+ * step -> EmptyDocument(index)).  *bad_index (host pointer, may be NULL) receives the first
+ * offending index (-1 if none); *bad_value (host, may be NULL) the offending entry.
+ */
+int mxs_validate_lens(const int32_t* valid_lens, int64_t n, int64_t l_pad, int64_t* bad_index, int64_t* bad_value,
+                      void* stream);
+int mxs_validate_cu_seqlens(const int64_t* cu_seqlens, int64_t n_docs, int64_t n_tokens, int64_t* bad_index,
+                            int64_t* bad_value, void* stream);
+
 /* Library identification. */
 const char* mxs_version(void);
 const char* mxs_status_string(int status);
@@ -63,9 +76,15 @@ int mxs_device_sm_count(void);
  *   argmax     [n_q, n_docs, l_q] int32, document-local, lowest index on ties; may be NULL:
  *              "rerank mode" -- the tensor-core kernels then keep only a running max per row
  *              (no index tracking; identical score bits, ~15 % faster at the ColPali shape)
- *   rowmax     [n_q, n_docs, l_q] float32 scratch/output (the per-token maxima)
+ *   rowmax     [n_q, n_docs, l_q] float32 per-token maxima, OPTIONAL (NULL: not materialised).
+ *              The tensor-core kernels fold S4 into their epilogue (score warp + cluster DSMEM)
+ *              whenever one CTA cluster holds a whole query (l_q <= 2048 for bf16/fp16 d = 128);
+ *              other shapes and the exact kernels run a separate S4 pass over the row maxima
+ *              (a stream-ordered scratch when rowmax is NULL).
  *   exact      0: tcgen05 tensor-core path (MXS_BF16 / MXS_F16; fp32 accumulation)
  *              1: bit-exact fp32 fold on CUDA cores (S1; any float dtype, required for MXS_F32)
+ * The kernels clamp valid_lens into [0, l_pad] (memory safety); out-of-range entries are a
+ * caller error detected by mxs_validate_lens (the reference raises, maxsim/forward.py:173-176).
  */
 int mxs_fused_score_batch(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs,
                           int64_t l_pad, int64_t dim, const int32_t* valid_lens, double* scores, int32_t* argmax,

@@ -17,8 +17,11 @@ LIB_DIR = os.path.join(PKG_DIR, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libmaxsim_b200.so")
 ROOT = os.path.dirname(PKG_DIR)
 
-# Translation units; each includes the kernel headers it instantiates.
-SOURCES = ["capi.cu"]
+# Translation units (compiled in parallel, then linked); each includes the kernel headers it
+# instantiates, and every kernel header is included by exactly one of them.
+SOURCES = ["host.cu", "capi.cu", "launch_ts_bf16.cu", "launch_ts_f16.cu", "launch_ts_i8.cu", "launch_ss.cu",
+           "launch_r3.cu", "launch_varlen.cu", "launch_exact.cu", "launch_bwd.cu", "launch_misc.cu"]
+OBJ_DIR = os.path.join(LIB_DIR, "obj")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -30,7 +33,7 @@ def _nvcc() -> str:
 
 
 def _inputs():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h"))]
     files.append(os.path.join(ROOT, "include", "maxsim_b200.h"))
     return files
 
@@ -42,32 +45,65 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
+def _obj(src: str) -> str:
+    return os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+
+
+def _deps(src: str):
+    """Dependencies of one TU from nvcc's -MD file (falls back to every source when absent)."""
+    dfile = _obj(src)[:-2] + ".d"
+    if not os.path.exists(dfile):
+        return None
+    text = open(dfile).read().replace("\\\n", " ")
+    _, _, rhs = text.partition(":")
+    return [d for d in rhs.split() if d]
+
+
+def _stale(src: str) -> bool:
+    obj = _obj(src)
+    if not os.path.exists(obj):
+        return True
+    deps = _deps(src)
+    if deps is None:
+        deps = _inputs()
+    t = os.path.getmtime(obj)
+    return any((not os.path.exists(d)) or os.path.getmtime(d) > t for d in deps)
+
+
+def _base_flags():
+    return [GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB_PATH
-    os.makedirs(LIB_DIR, exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    nvcc = _nvcc()
+    todo = [s for s in SOURCES if force or _stale(s)]
+    procs = []
+    for src in todo:
+        obj = _obj(src)
+        cmd = [nvcc] + _base_flags() + ["-MD", "-MF", obj[:-2] + ".d", "-c", os.path.join(CSRC, src), "-o", obj + ".tmp"]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    errs = []
+    for src, obj, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            errs.append(f"nvcc failed on {src} ({pr.returncode}):\n{out}\n{err}")
+        else:
+            os.replace(obj + ".tmp", obj)
+            if verbose and err:
+                print(err, file=sys.stderr)
+    if errs:
+        raise RuntimeError("\n".join(errs))
     tmp = LIB_PATH + ".tmp"
-    cmd = [
-        _nvcc(),
-        GENCODE,
-        "-O3",
-        "-lineinfo",
-        "-std=c++17",
-        "-Xcompiler",
-        "-fPIC",
-        "-shared",
-        "-I" + os.path.join(ROOT, "include"),
-        "-o",
-        tmp,
-    ] + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
+    cmd = [nvcc, GENCODE, "-shared", "-Xcompiler", "-fPIC", "-Xlinker", "--no-undefined", "-o", tmp] + [_obj(s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        print(res.stderr, file=sys.stderr)
+        raise RuntimeError(f"link failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -52,6 +52,8 @@ _SIGNATURES = {
     "mxs_mxs1_read_block": [c_vp, c_i64, c_i64, c_vp, c_size],
     "mxs_mxs1_read_scales": [c_vp, c_vp, c_size],
     "mxs_mxs1_close": [c_vp],
+    "mxs_validate_lens": [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "mxs_validate_cu_seqlens": [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
 }
 _RESTYPES = {
     "mxs_version": ctypes.c_char_p,

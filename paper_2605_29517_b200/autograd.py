@@ -36,10 +36,10 @@ class MaxSimFunction(torch.autograd.Function):
     """scores[q, b] = sum_i max_{j < valid_len[b]} <Q[q, i], D[b, j]>  (float64 output)."""
 
     @staticmethod
-    def forward(ctx, Q, D, valid_lens=None, exact=None):
+    def forward(ctx, Q, D, valid_lens=None, exact=None, validate=True):
         from .forward import score_dense
 
-        scores, argmax, _ = score_dense(Q.detach(), D.detach(), valid_lens, exact=exact)
+        scores, argmax, _ = score_dense(Q.detach(), D.detach(), valid_lens, exact=exact, validate=validate)
         ctx.save_for_backward(Q, D, argmax)
         ctx.mark_non_differentiable(argmax)
         return scores, argmax
@@ -59,17 +59,17 @@ class MaxSimFunction(torch.autograd.Function):
             off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
             lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
             dD = _grad_docs(Qc, argmax, g, off, lens, b * l_pad, l_pad, dim).reshape(b, l_pad, dim).to(D.dtype)
-        return dQ, dD, None, None
+        return dQ, dD, None, None, None
 
 
 class MaxSimVarlenFunction(torch.autograd.Function):
     """Packed-corpus variant: tokens [T, d] delimited by cu_seqlens (int64 [B + 1], CUDA)."""
 
     @staticmethod
-    def forward(ctx, Q, tokens, cu_dev, max_doc_len, exact=None):
+    def forward(ctx, Q, tokens, cu_dev, max_doc_len, exact=None, validate=True):
         from .varlen import score_varlen
 
-        scores, argmax, _ = score_varlen(Q.detach(), tokens.detach(), cu_dev, exact=exact)
+        scores, argmax, _ = score_varlen(Q.detach(), tokens.detach(), cu_dev, exact=exact, validate=validate)
         ctx.save_for_backward(Q, tokens, cu_dev, argmax)
         ctx.max_doc_len = int(max_doc_len)
         ctx.mark_non_differentiable(argmax)
@@ -88,19 +88,24 @@ class MaxSimVarlenFunction(torch.autograd.Function):
             lens = (cu[1:] - cu[:-1]).contiguous()
             Qc = Q.detach().to(tokens.dtype).contiguous()
             dT = _grad_docs(Qc, argmax, g, off, lens, tokens.shape[0], ctx.max_doc_len, dim).to(tokens.dtype)
-        return dQ, dT, None, None, None
+        return dQ, dT, None, None, None, None
 
 
-def maxsim(Q: torch.Tensor, D: torch.Tensor, valid_lens: torch.Tensor | None = None, exact=None):
-    """Differentiable MaxSim: Q [N_q, L_q, d], D [B, L, d] -> scores f64 [N_q, B]."""
-    scores, _ = MaxSimFunction.apply(Q, D, valid_lens, exact)
+def maxsim(Q: torch.Tensor, D: torch.Tensor, valid_lens: torch.Tensor | None = None, exact=None, validate=True):
+    """Differentiable MaxSim: Q [N_q, L_q, d], D [B, L, d] -> scores f64 [N_q, B].
+
+    valid_lens entries must lie in [1, L] (EmptyDocument / ShapeMismatch otherwise, one device
+    check; validate=False skips it, e.g. inside CUDA graphs)."""
+    scores, _ = MaxSimFunction.apply(Q, D, valid_lens, exact, validate)
     return scores
 
 
-def maxsim_varlen(Q: torch.Tensor, tokens: torch.Tensor, cu_seqlens, exact=None):
+def maxsim_varlen(Q: torch.Tensor, tokens: torch.Tensor, cu_seqlens, exact=None, validate=True):
     """Differentiable packed MaxSim: Q [N_q, L_q, d], tokens [T, d], cu_seqlens [B + 1]."""
     cu = cu_seqlens if isinstance(cu_seqlens, torch.Tensor) else torch.as_tensor(cu_seqlens)
-    max_len = int((cu[1:] - cu[:-1]).max().item())
     cu = cu.to(device=tokens.device, dtype=torch.int64).contiguous()
-    scores, _ = MaxSimVarlenFunction.apply(Q, tokens, cu, max_len, exact)
+    if validate:
+        _dev.validate_cu(cu, tokens.shape[0])
+    max_len = int((cu[1:] - cu[:-1]).max().item())
+    scores, _ = MaxSimVarlenFunction.apply(Q, tokens, cu, max_len, exact, False)
     return scores

@@ -11,9 +11,7 @@
 // chunks of 64 (the fold order over k is preserved across chunks).  Four k steps per LDS.128
 // (query row and the 8 broadcast document rows); one rounding per product and per add, in k order.
 #pragma once
-#include "ptx.cuh"
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
+#include "convert.cuh"
 
 namespace mxs {
 
@@ -27,15 +25,6 @@ struct FwdExactParams {
 
 constexpr int kExRows = 32, kExCols = 64, kExK = 64, kExThreads = 256;
 constexpr int kExStride = kExK + 4;  // row pitch in floats: 16-B aligned rows, conflict-free LDS.128
-
-template <typename T>
-MXS_DEV float to_f32(T x);
-template <>
-MXS_DEV float to_f32<float>(float x) { return x; }
-template <>
-MXS_DEV float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
-template <>
-MXS_DEV float to_f32<__half>(__half x) { return __half2float(x); }
 
 // rows x kw elements of a row-major [*, dim] operand starting at (row0, k0) -> smem [rows][kExStride],
 // zero outside (rows_valid, kw).  fp32 with dim % 4 == 0: float4 loads.
@@ -91,7 +80,7 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_kernel(const T* __res
       vl = (int)(p.cu_seqlens[b + 1] - drow0);
     } else {
       drow0 = (long long)b * p.l_pad;
-      vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+      vl = p.valid_lens ? min(max(p.valid_lens[b], 0), p.l_pad) : p.l_pad;  // clamped: memory-safe on unvalidated input
     }
     const T* qbase = Q + (long long)q * p.l_q * p.dim;
     const T* dbase = D + drow0 * p.dim;
@@ -205,7 +194,7 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_f32v_kernel(const flo
       vl = (int)(p.cu_seqlens[b + 1] - drow0);
     } else {
       drow0 = (long long)b * p.l_pad;
-      vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+      vl = p.valid_lens ? min(max(p.valid_lens[b], 0), p.l_pad) : p.l_pad;  // clamped: memory-safe on unvalidated input
     }
     const float* qbase = Q + (long long)q * p.l_q * p.dim;
     const float* dbase = D + drow0 * p.dim;
@@ -315,7 +304,7 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_i8_kernel(const int8_
   const long long n_pairs = (long long)p.n_q * p.n_docs;
   for (long long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
     const int q = (int)(pr / p.n_docs), b = (int)(pr % p.n_docs);
-    const int vl = p.valid_lens ? p.valid_lens[b] : p.l_pad;
+    const int vl = p.valid_lens ? min(max(p.valid_lens[b], 0), p.l_pad) : p.l_pad;  // clamped: memory-safe on unvalidated input
     const int8_t* qbase = Q + (long long)q * p.l_q * p.dim;
     const int8_t* dbase = D + (long long)b * p.l_pad * p.dim;
     for (int r0 = 0; r0 < p.l_q; r0 += kExRows) {
@@ -374,54 +363,6 @@ __global__ void __launch_bounds__(kExThreads, 3) fwd_exact_i8_kernel(const int8_
       }
       __syncthreads();
     }
-  }
-}
-
-// Per-pair score: the strict left-to-right float64 sum of the fp32 row maxima (S4,
-// `maxsim/kernels.py:22-26` seq_sum_f64), computed in parallel when that is provably identical.
-//
-// Every fp32 value is a multiple of its ulp 2^(E-150) (E = biased exponent, 1 for subnormals)
-// and smaller than 2^(E-126).  If Emax - Emin <= 29 - ceil(log2 n), every partial sum of any
-// subset is a multiple of 2^(Emin-150) below 2^(53+Emin-150): exactly representable in f64.
-// Then the sequential sum and any tree sum are both the exact sum -- bit-identical.  Pairs that
-// fail the certificate (maxima spanning > 2^19 in magnitude) take the sequential chain.
-// One warp per pair; lanes stride the row maxima (coalesced).
-__global__ void rowsum_kernel(const float* __restrict__ rowmax, long long n_pairs, int l_q, double* __restrict__ scores) {
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= n_pairs) return;
-  const float* r = rowmax + warp * l_q;
-  double s = 0.0;
-  int emin = 255, emax = 0;
-  bool finite = true;
-  for (int i = lane; i < l_q; i += 32) {
-    const float v = __ldg(r + i);
-    const uint32_t bits = __float_as_uint(v) & 0x7fffffffu;
-    if (bits >= 0x7f800000u) finite = false;
-    if (bits != 0u) {
-      const int e = max((int)(bits >> 23), 1);
-      emin = min(emin, e);
-      emax = max(emax, e);
-    }
-    s += (double)v;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-  }
-  finite = __all_sync(0xffffffffu, finite);
-  const int log2n = 32 - __clz(max(l_q - 1, 1));
-  const bool exact = finite && (emax == 0 || emax - emin <= 29 - log2n);
-  if (exact) {
-    if (lane == 0) scores[warp] = s;
-    return;
-  }
-  if (lane == 0) {  // sequential fallback (rare): the reference order itself
-    double t = (double)r[0];
-    for (int i = 1; i < l_q; ++i) t = __dadd_rn(t, (double)r[i]);
-    scores[warp] = t;
   }
 }
 

@@ -25,7 +25,8 @@ namespace mxs {
 
 constexpr int kR8Sets = 3;
 constexpr int kR8EpiWarps = 4 * kR8Sets;
-constexpr int kR8Threads = 32 * (2 + kR8EpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM, 2..13 epilogue
+constexpr int kR8SumWarp = 2 + kR8EpiWarps;          // warp 14: fused S4 score (as in fwd_ts.cuh)
+constexpr int kR8Threads = 32 * (kR8SumWarp + 1);  // warp 0 TMA, warp 1 MMA + TMEM, 2..13 epilogue
 constexpr int kR8AccCol0 = 128;
 
 constexpr int kR8PartBufs = 4;  // per-document partial-maximum buffers in flight
@@ -41,15 +42,17 @@ struct R8SmemHeader {
   uint64_t qempty;
   uint64_t sfull[kScaleSlots];
   uint64_t sempty[kScaleSlots];
+  uint64_t sready[2];  // fused score row buffers (rank 0), see fwd_ts.cuh
+  uint64_t sfree[2];
   uint32_t tmem_base;
   uint32_t pad;
 };
 
 // dynamic smem: document tiles + per-document partial maxima [4 docs][3 sets][4 blocks][128 rows]
-// + (INT8) the scale ring and the bias tile
-__host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages, bool i8) {
+// + (INT8) the scale ring and the bias tile + the fused-score row buffers (2 x sum_rows floats)
+__host__ __device__ inline size_t fwd_i8r_smem_bytes(int ka, int stages, bool i8, int sum_rows) {
   return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)kR8PartBufs * kR8Sets * 4 * 128 * sizeof(float) +
-         (i8 ? (size_t)kScaleSlots * kTileRows * sizeof(float) + kBiasTileBytes : 0);
+         (i8 ? (size_t)kScaleSlots * kTileRows * sizeof(float) + kBiasTileBytes : 0) + (size_t)2 * sum_rows * sizeof(float);
 }
 
 template <TcKind KIND, int KA, int CL>
@@ -62,6 +65,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   float* sPart = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
   float* sScale = sPart + (size_t)kR8PartBufs * kR8Sets * 4 * 128;
   uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + kScaleSlots * kTileRows);  // 1024-B aligned
+  float* sSum = (KIND == TcKind::I8) ? reinterpret_cast<float*>(sBias + kBiasTileBytes) : sScale;
+  const bool fuse = p.scores != nullptr && !(KIND != TcKind::I8 && p.debug == 3);
   __shared__ R8SmemHeader r8_hdr;
   R8SmemHeader* hdr = &r8_hdr;
 
@@ -104,6 +109,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     for (int s = 0; s < kScaleSlots; ++s) {
       mbar_init(&hdr->sfull[s], 1);
       mbar_init(&hdr->sempty[s], kR8EpiWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&hdr->sready[s], 32 * 4 * CL);  // the four quadrant combiners of every CTA, all lanes
+      mbar_init(&hdr->sfree[s], 1);
     }
     fence_mbar_init();
   }
@@ -230,6 +239,21 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       if (elect_one()) mma_commit(&hdr->qempty);
       __syncwarp();
       mbar_wait(&hdr->qempty, qphase ^ 1u);
+    }
+  } else if (warp == kR8SumWarp) {
+    // ------------------------------------------------------------------ fused S4 score (rank 0)
+    if (fuse && crank == 0) {
+      uint32_t n = 0;
+      for (long long u = u_begin; u < u_end; ++u, ++n) {
+        int q, g, b;
+        decode(u, q, g, b);
+        const uint32_t sb = n & 1u;
+        mbar_wait_cl<CL>(&hdr->sready[sb], (n >> 1) & 1u);
+        const double sc = warp_score_sum(sSum + sb * p.sum_rows, p.l_q);
+        if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
+        __syncwarp();
+        if (lane < (uint32_t)CL) mbar_arrive_rank<CL>(&hdr->sfree[sb], lane);
+      }
     }
   } else {
     // ------------------------------------------------------------------ epilogue sets
@@ -375,12 +399,18 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         __threadfence_block();
         const volatile float* vb = buf;
         const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
+        const uint32_t sb = ndoc & 1u;
+        if (fuse) mbar_wait_cl<CL>(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
         for (int mb = 0; mb < qbv; ++mb) {
           const int row = (g * p.qb + mb) * kTileRows + row_local;
           const float m = fmaxf(fmaxf(vb[(0 * 4 + mb) * 128 + row_local], vb[(1 * 4 + mb) * 128 + row_local]),
                                 vb[(2 * 4 + mb) * 128 + row_local]);
-          if (row < p.l_q) p.rowmax[obase + row] = m;
+          if (row < p.l_q) {
+            if (p.rowmax) p.rowmax[obase + row] = m;
+            if (fuse) st_rank0_f32<CL>(sSum + sb * p.sum_rows + row, m);
+          }
         }
+        if (fuse) mbar_arrive_rank<CL>(&hdr->sready[sb], 0u);
         __syncwarp();
         if (lane == 0) {
           hdr->pcnt[pb][quad] = 0u;

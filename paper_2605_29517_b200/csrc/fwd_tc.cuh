@@ -16,10 +16,10 @@
 // fold them into register-resident running (max, argmax) per Q row.
 #pragma once
 #include "ptx.cuh"
+#include "kinds.h"
 
 namespace mxs {
 
-enum class TcKind : int { BF16 = 0, F16 = 1, I8 = 2 };
 
 struct FwdTcParams {
   int n_q, l_q, n_docs, l_pad, dim;
@@ -36,6 +36,8 @@ struct FwdTcParams {
   int debug;                  // profiling knobs (MXS_DEBUG env): 1 = skip fold, 2 = skip TMEM loads too
   int mma_spin;               // MXS_MMA_SPIN=1: the MMA issuer spins (no suspend) on accumulator-slot waits
   const void* q_ptr;          // Q rows in global memory (TS kernel loads them into TMEM)
+  double* scores;             // [n_q, n_docs]: fused S4 sum in the epilogue (fwd_ts / fwd_i8r), or nullptr
+  int sum_rows;               // row capacity of each shared-memory row-maxima buffer (fused sum)
 };
 
 constexpr int kTileRows = 128;     // rows per Q block and per document tile
@@ -69,7 +71,8 @@ MXS_DEV void decode_unit(long long u, const FwdTcParams& p, int& q, int& g, int&
 }
 
 MXS_DEV int doc_valid_len(const FwdTcParams& p, int b) {
-  return p.valid_lens ? __ldg(p.valid_lens + b) : p.l_pad;
+  // clamped into [0, l_pad] so that unvalidated input can never address another document's rows
+  return p.valid_lens ? min(max(__ldg(p.valid_lens + b), 0), p.l_pad) : p.l_pad;
 }
 
 // max of 32 values as a 3-input tree (FMNMX3): 15 ALU instructions, depth 4.

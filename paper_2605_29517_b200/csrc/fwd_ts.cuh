@@ -13,15 +13,22 @@
 //     copy of the improving 32-column chunk in shared memory.  The lowest index attaining the
 //     final max is resolved once per (row, document) from that copy -- no per-chunk rescans
 //     across the warp.
+//   * fused S4 score: at the end of a document every epilogue thread stores its row maxima into a
+//     double-buffered row array in the shared memory of cluster rank 0 (DSMEM stores for the
+//     other ranks) and arrives on that buffer's mbarrier; a dedicated score warp of rank 0 folds
+//     the L_q maxima with the certified f64 sum (score_sum.cuh) and writes the score, so the
+//     [N_q, B, L_q] row maxima never reach HBM (they are written only on request).
 #pragma once
 #include "fwd_tc.cuh"
+#include "score_sum.cuh"
 
 namespace mxs {
 
 constexpr int kTsAccCol0 = 256;  // accumulator slots start here
 constexpr int kTsSlots = 2;
 constexpr int kTsEpiWarp0 = 2;                               // warps 2..9: epilogue
-constexpr int kTsThreads = 32 * (kTsEpiWarp0 + kEpiWarps);  // warp 0 TMA, warp 1 MMA + TMEM alloc
+constexpr int kTsSumWarp = kTsEpiWarp0 + kEpiWarps;          // warp 10: fused S4 score
+constexpr int kTsThreads = 32 * (kTsSumWarp + 1);  // warp 0 TMA, warp 1 MMA + TMEM alloc
 constexpr int kScaleSlots = 8;  // INT8: ring of per-tile document scales (128 f32 each) in smem
 
 struct TsSmemHeader {
@@ -33,6 +40,8 @@ struct TsSmemHeader {
   uint64_t qempty;
   uint64_t sfull[kScaleSlots];   // INT8 scale ring: TMA bulk copy landed
   uint64_t sempty[kScaleSlots];  // INT8 scale ring: all 8 epilogue warps done with the tile
+  uint64_t sready[2];            // fused score: a document's row maxima are in row buffer [doc & 1] (rank 0)
+  uint64_t sfree[2];             // fused score: rank 0's score warp has consumed row buffer [doc & 1]
   uint32_t tmem_base;
   uint32_t pad;
 };
@@ -54,11 +63,14 @@ MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
 }
 
 
-// dynamic shared memory (the header is static shared memory); `scales` adds the INT8 scale ring,
-// `bias` the ring's space (used or not) plus the INT8 bias tile after it
-__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales = false, bool bias = false) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (size_t)qb * 128 * 128 +
-         ((scales || bias) ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0) + (bias ? kBiasTileBytes : 0);
+// dynamic shared memory (the header is static shared memory): document-tile ring | argmax stash
+// (`stash`: 32 floats per Q row) | INT8 scale ring (`scales`, or reserved when `bias`) | INT8 bias
+// tile (`bias`) | fused-score row buffers (2 x `sum_rows` floats)
+__host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales, bool bias, bool stash,
+                                                    int sum_rows) {
+  return 1024 + (size_t)stages * ka * kAtomBytes + (stash ? (size_t)qb * 128 * 128 : 0) +
+         ((scales || bias) ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0) + (bias ? kBiasTileBytes : 0) +
+         (size_t)2 * sum_rows * sizeof(float);
 }
 
 // Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
@@ -210,11 +222,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint8_t* sD = smem;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
   // INT8 scale ring (only when d_scale rows are 16-B aligned: l_pad % 4 == 0)
-  float* sScale = sBest + (size_t)p.qb * 128 * 32;
+  float* sScale = sBest + (p.argmax ? (size_t)p.qb * 128 * 32 : 0);
   const bool scale_ring = (KIND == TcKind::I8) && ((p.l_pad & 3) == 0);
   // INT8 with |acc| <= 2^22 (d <= 256): accumulators pre-biased to kMagicF (see fill_bias_tile)
   constexpr bool kBias = (KIND == TcKind::I8) && (KA <= 2);
-  uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + kScaleSlots * kTileRows);
+  uint8_t* sBias = reinterpret_cast<uint8_t*>(sScale + ((scale_ring || kBias) ? kScaleSlots * kTileRows : 0));
+  float* sSum = reinterpret_cast<float*>(sBias + (kBias ? kBiasTileBytes : 0));
+  // fused S4 score (the profiling knob MXS_DEBUG=3 skips the drain, so it has nothing to sum)
+  const bool fuse = p.scores != nullptr && !(KIND != TcKind::I8 && p.debug == 3);
   __shared__ TsSmemHeader ts_hdr;  // static shared: keeps barrier / bookkeeping accesses on LDS/STS
   TsSmemHeader* hdr = &ts_hdr;
 
@@ -256,6 +271,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     for (int s = 0; s < kScaleSlots; ++s) {
       mbar_init(&hdr->sfull[s], 1);
       mbar_init(&hdr->sempty[s], kEpiWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&hdr->sready[s], 32 * kEpiWarps * CL);  // every epilogue lane of the cluster
+      mbar_init(&hdr->sfree[s], 1);
     }
     fence_mbar_init();
   }
@@ -393,6 +412,21 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       __syncwarp();
       mbar_wait(&hdr->qempty, qphase ^ 1u);
     }
+  } else if (warp == kTsSumWarp) {
+    // ------------------------------------------------------------------ fused S4 score (rank 0)
+    if (fuse && crank == 0) {
+      uint32_t n = 0;
+      for (long long u = u_begin; u < u_end; ++u, ++n) {
+        int q, g, b;
+        decode(u, q, g, b);
+        const uint32_t sb = n & 1u;
+        mbar_wait_cl<CL>(&hdr->sready[sb], (n >> 1) & 1u);
+        const double sc = warp_score_sum(sSum + sb * p.sum_rows, p.l_q);
+        if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
+        __syncwarp();
+        if (lane < (uint32_t)CL) mbar_arrive_rank<CL>(&hdr->sfree[sb], lane);
+      }
+    }
   } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
     // warp w in [2, 10): TMEM lane quadrant w % 4 (hardware rule), set (w - 2) / 4.
@@ -405,6 +439,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int row_bytes = p.dim * eb;
     uint32_t sph = 0, qeph = 0;  // this set's slot is `wset`; sph = parity of its next use
     uint32_t sc_n = 0;           // tiles consumed from the scale ring
+    uint32_t ndoc = 0;           // documents finished (fused-score row buffer = ndoc & 1)
     long long cur_key = -1;
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
@@ -575,13 +610,26 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         if (mb >= qbv) break;
         const int row = (g * p.qb + mb) * kTileRows + row_local;
         if (row < p.l_q) {
-          p.rowmax[obase + row] = m[i];
+          if (p.rowmax) p.rowmax[obase + row] = m[i];
           if (p.argmax) {
             float w[32];
             unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * 32, w, swz);
-            p.argmax[obase + row] = cb[i] + first_argmax32_chain(w, m[i]);
+            p.argmax[obase + row] = ntiles ? cb[i] + first_argmax32_chain(w, m[i]) : 0;  // 0: empty (invalid) doc
           }
         }
+      }
+      if (fuse) {  // row maxima -> rank 0's row buffer, then every lane arrives (release, cluster scope)
+        const uint32_t sb = ndoc & 1u;
+        mbar_wait_cl<CL>(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
+        float* dst = sSum + sb * p.sum_rows;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int mb = 2 * i + wset;
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          if (mb < qbv && row < p.l_q) st_rank0_f32<CL>(dst + row, m[i]);
+        }
+        mbar_arrive_rank<CL>(&hdr->sready[sb], 0u);
+        ++ndoc;
       }
     }
   }

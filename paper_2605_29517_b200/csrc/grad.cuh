@@ -6,7 +6,7 @@
 // the reference's order (maxsim/backward.py:165-172, :225-231) and stores it exactly once -- no
 // atomics anywhere.  Lanes split the embedding axis (VEC contiguous elements per lane).
 #pragma once
-#include "fwd_exact.cuh"  // to_f32
+#include "convert.cuh"  // to_f32
 
 namespace mxs {
 

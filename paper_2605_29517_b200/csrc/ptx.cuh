@@ -287,6 +287,57 @@ MXS_DEV void i2f2_magic(float& o0, float& o1, uint32_t a0, uint32_t a1) {
 MXS_DEV void i2f2_biased(float& o0, float& o1, uint32_t a0, uint32_t a1) {
   fadd2_rn(o0, o1, __uint_as_float(a0), __uint_as_float(a1), -kMagicF, -kMagicF);
 }
+// ---------------------------------------------------------------- distributed shared memory
+// Address of the same shared variable in CTA `rank` of the cluster (shared::cluster window).
+MXS_DEV uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+MXS_DEV void st_cluster_f32(uint32_t cluster_addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
+}
+// Arrive (release at cluster scope) on an mbarrier that may live in another CTA of the cluster.
+MXS_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Wait on a local mbarrier whose arrivals come from other CTAs (acquire at cluster scope).
+MXS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+// Cluster-size-generic forms: CL == 1 stays on the CTA-local instructions.
+template <int CL>
+MXS_DEV void st_rank0_f32(float* local_ptr, float v) {
+  if constexpr (CL == 1)
+    *local_ptr = v;
+  else
+    st_cluster_f32(mapa_u32(smem_u32(local_ptr), 0u), v);
+}
+template <int CL>
+MXS_DEV void mbar_arrive_rank(uint64_t* local_bar, uint32_t rank) {
+  if constexpr (CL == 1)
+    mbar_arrive(local_bar);
+  else
+    mbar_arrive_cluster(mapa_u32(smem_u32(local_bar), rank));
+}
+template <int CL>
+MXS_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  if constexpr (CL == 1)
+    mbar_wait(bar, parity);
+  else
+    mbar_wait_cluster(bar, parity);
+}
+
 MXS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

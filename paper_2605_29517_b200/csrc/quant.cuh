@@ -3,7 +3,7 @@
 //   q     = clamp(rint_half_even(fl32(x / scale)), -levels, levels)
 // One warp per row; IEEE division (__fdiv_rn) and rintf, no fast-math.
 #pragma once
-#include "fwd_exact.cuh"  // to_f32
+#include "convert.cuh"  // to_f32
 
 namespace mxs {
 

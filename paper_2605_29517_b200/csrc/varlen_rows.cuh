@@ -19,8 +19,12 @@
 // CTAs own contiguous, token-balanced document ranges (binary search of cu_seqlens on the
 // device), so every document is finished by exactly one CTA: no atomics, no second pass.
 // HBM-bound: L_q = 32 gives 32 FLOP/B; the MMA is a fraction of the per-tile HBM time.
+// Fused S4 score (query length dividing 32): every emission site is warp-uniform and a warp holds
+// 32 consecutive query rows, so the L_q maxima of a (query, document) pair meet in one warp and
+// are folded there by a segmented certified f64 sum (score_sum.cuh) -- no row maxima in HBM.
 #pragma once
 #include "fwd_tc.cuh"
+#include "score_sum.cuh"
 
 namespace mxs {
 
@@ -32,8 +36,9 @@ struct VarlenRowsParams {
   int dim;
   int stages;
   const long long* cu;  // [n_docs + 1] device
-  float* rowmax;        // [n_q, n_docs, l_q]
+  float* rowmax;        // [n_q, n_docs, l_q] or nullptr (fused score)
   int32_t* argmax;      // [n_q, n_docs, l_q] or nullptr
+  double* scores;       // [n_q, n_docs]: fused S4 score (l_q divides 32), or nullptr
 };
 
 constexpr int kVrTile = 128;       // tokens per tile (MMA N)
@@ -97,10 +102,42 @@ MXS_DEV long long vr_row_base(const VarlenRowsParams& p, int row) {
   const int q = r / p.l_q, i = r - q * p.l_q;
   return (long long)q * p.n_docs * p.l_q + i;
 }
+// Whole warp (warp-uniform doc): S4 score of every query whose l_q rows are lanes
+// [k * l_q, (k + 1) * l_q) of the warp.  Lanes without a row (rbase < 0) contribute nothing.
+__device__ __noinline__ void vr_emit_score(const VarlenRowsParams& p, long long rbase, long long doc, float m) {
+  if (doc < 0) return;
+  const int lane = (int)(threadIdx.x & 31u);
+  const int seg = p.l_q;  // power of two <= 32
+  const bool valid = rbase >= 0;
+  CertSum c;
+  if (valid) c.add(m);
+  int fin = c.finite ? 1 : 0;
+  for (int o = seg >> 1; o; o >>= 1) {  // segmented butterfly: xor offsets < seg stay in the segment
+    c.s += __shfl_xor_sync(0xffffffffu, c.s, o);
+    c.emin = min(c.emin, __shfl_xor_sync(0xffffffffu, c.emin, o));
+    c.emax = max(c.emax, __shfl_xor_sync(0xffffffffu, c.emax, o));
+    fin = min(fin, __shfl_xor_sync(0xffffffffu, fin, o));
+  }
+  c.finite = fin != 0;
+  const bool lead = valid && (lane & (seg - 1)) == 0;
+  const bool ex = c.exact(seg);
+  double sc = c.s;
+  if (__any_sync(0xffffffffu, lead && !ex)) {  // sequential chain (rare): the reference order
+    double t = 0.0;
+    for (int i = 0; i < seg; ++i) {
+      const float v = __shfl_sync(0xffffffffu, m, (lane & ~(seg - 1)) + i);
+      t = (i == 0) ? (double)v : __dadd_rn(t, (double)v);
+    }
+    if (!ex) sc = t;
+  }
+  if (lead) p.scores[rbase / ((long long)p.n_docs * p.l_q) * p.n_docs + doc] = sc;
+}
+
 MXS_DEV void vr_emit(const VarlenRowsParams& p, long long rbase, long long doc, float m, long long arg_local) {
+  if (p.scores) vr_emit_score(p, rbase, doc, m);
   if (rbase < 0 || doc < 0) return;
   const long long o = rbase + doc * p.l_q;
-  p.rowmax[o] = m;
+  if (p.rowmax) p.rowmax[o] = m;
   if (p.argmax) p.argmax[o] = (int32_t)arg_local;
 }
 

@@ -91,11 +91,15 @@ def use_exact_path(dtype: torch.dtype, dim: int, exact: bool | None) -> bool:
 
 
 def score_dense(Q: torch.Tensor, D: torch.Tensor, valid_lens: torch.Tensor | None = None, *, exact: bool | None = None,
-                want_argmax: bool = True, out=None, stream=None):
+                want_argmax: bool = True, want_rowmax: bool = False, out=None, stream=None, validate: bool = True):
     """Tensor-level dense forward: Q [n_q, l_q, d], D [B, L_pad, d] on CUDA.
 
-    Returns (scores f64 [n_q, B], argmax int32 [n_q, B, l_q] or None, rowmax f32 [n_q, B, l_q]).
-    `out` may supply preallocated (scores, argmax, rowmax) buffers (CUDA-graph friendly).
+    Returns (scores f64 [n_q, B], argmax int32 [n_q, B, l_q] or None, rowmax f32 [n_q, B, l_q] or None).
+    The per-token maxima are materialised only with want_rowmax=True (the tensor-core kernels fold
+    the f64 score into their epilogue).  `out` may supply preallocated (scores, argmax, rowmax)
+    buffers (CUDA-graph friendly; argmax / rowmax entries may be None).  With validate=True (the
+    default) device-resident valid_lens are checked like maxsim/forward.py:173-176 (one sync);
+    callers holding validated lengths (DocBatch, graphs) pass validate=False.
     """
     _dev.require_cuda(Q, D, valid_lens)
     if Q.dim() != 3 or D.dim() != 3:
@@ -111,17 +115,25 @@ def score_dense(Q: torch.Tensor, D: torch.Tensor, valid_lens: torch.Tensor | Non
     Q = Q.contiguous()
     D = D.contiguous()
     exact_path = use_exact_path(D.dtype, int(d), exact)
-    if out is not None:
-        scores, argmax, rowmax = out
-    else:
-        scores = torch.empty((n_q, b), dtype=torch.float64, device=D.device)
-        argmax = torch.empty((n_q, b, l_q), dtype=torch.int32, device=D.device) if want_argmax else None
-        rowmax = torch.empty((n_q, b, l_q), dtype=torch.float32, device=D.device)
-    if valid_lens is not None and valid_lens.dtype != torch.int32:
-        valid_lens = valid_lens.to(torch.int32)
-    _lib.call("mxs_fused_score_batch", _dev.dtype_code(D), _dev.ptr(Q), n_q, l_q, _dev.ptr(D), b, l_pad, d,
-              _dev.ptr(valid_lens), _dev.ptr(scores), _dev.ptr(argmax), _dev.ptr(rowmax), 1 if exact_path else 0,
-              _dev.stream_handle(stream))
+    with _dev.on_device(D):
+        if valid_lens is not None:
+            if valid_lens.dtype != torch.int32 or not valid_lens.is_contiguous():
+                valid_lens = valid_lens.to(torch.int32).contiguous()
+            if valid_lens.numel() != b:
+                raise ShapeMismatch(f"valid_lens holds {valid_lens.numel()} entries for {b} documents")
+            if validate:
+                _dev.validate_lens(valid_lens, l_pad, stream)
+        if out is not None:
+            scores, argmax, rowmax = out
+        else:
+            scores = torch.empty((n_q, b), dtype=torch.float64, device=D.device)
+            argmax = torch.empty((n_q, b, l_q), dtype=torch.int32, device=D.device) if want_argmax else None
+            rowmax = torch.empty((n_q, b, l_q), dtype=torch.float32, device=D.device) if want_rowmax else None
+        for t in (Q, D, valid_lens):
+            _dev.keep_alive(t, stream)
+        _lib.call("mxs_fused_score_batch", _dev.dtype_code(D), _dev.ptr(Q), n_q, l_q, _dev.ptr(D), b, l_pad, d,
+                  _dev.ptr(valid_lens), _dev.ptr(scores), _dev.ptr(argmax), _dev.ptr(rowmax), 1 if exact_path else 0,
+                  _dev.stream_handle(stream, D.device))
     return scores, argmax, rowmax
 
 
@@ -179,9 +191,9 @@ def fused_score_batch(queries, docs, tile: TileConfig = DEFAULT_TILE, report: Tr
     if Q.dtype != docs.data.dtype:
         Q = Q.to(docs.data.dtype)
     n_q, l_q, d = Q.shape
-    scores, argmax, rowmax = score_dense(Q, docs.data, docs.valid_lens, exact=exact)
-    rep.alloc(rowmax.numel() * 4)
-    rep.release(rowmax.numel() * 4)
+    scores, argmax, _ = score_dense(Q, docs.data, docs.valid_lens, exact=exact, validate=False)
+    rep.alloc(n_q * docs.n_docs * l_q * 4)  # per-token maxima (registers / shared memory on the device)
+    rep.release(n_q * docs.n_docs * l_q * 4)
     _account_dense(rep, n_q, l_q, docs.n_docs, docs.padded_len, d, _dev.itemsize(docs.data), count_query)
     am = ArgmaxMap(argmax, docs.valid_lens_host, padded_len=docs.padded_len, validate=False)
     return ScoreMatrix(scores, validate=False), am, rep
@@ -203,6 +215,6 @@ def fused_score_pair(query, doc, valid_len: int | None = None, tile: TileConfig 
     D = dm.data[None]
     vl = torch.tensor([valid_len], dtype=torch.int32, device=D.device)
     Q = q.data[None].to(D.dtype)
-    scores, argmax, _ = score_dense(Q, D, vl, exact=exact)
+    scores, argmax, _ = score_dense(Q, D, vl, exact=exact, validate=False)
     _account_dense(rep, 1, q.rows, 1, dm.rows, dm.dim, _dev.itemsize(D), True)
     return float(scores[0, 0].item()), argmax[0, 0], rep

@@ -132,22 +132,36 @@ def dequantize(qm: QuantizedMatrix) -> torch.Tensor:
     return qm.scale[:, None] * qm.q.to(torch.float32)
 
 
-def score_int8(q_q, q_s, d_q, d_s, valid_lens=None, want_argmax=True, stream=None):
-    """Tensor-level batched INT8 forward: q_q [n_q, l_q, d] i8, q_s [n_q, l_q]; d_q [B, L, d], d_s [B, L]."""
+def score_int8(q_q, q_s, d_q, d_s, valid_lens=None, want_argmax=True, stream=None, *, want_rowmax=False,
+               validate=True):
+    """Tensor-level batched INT8 forward: q_q [n_q, l_q, d] i8, q_s [n_q, l_q]; d_q [B, L, d], d_s [B, L].
+
+    Returns (scores f64 [n_q, B], argmax or None, rowmax or None) -- see forward.score_dense.
+    """
     _dev.require_cuda(q_q, d_q)
     n_q, l_q, dim = q_q.shape
     b, l_pad, d2 = d_q.shape
     if dim != d2:
         raise DimMismatch(int(dim), int(d2))
+    if tuple(q_s.shape) != (n_q, l_q) or tuple(d_s.shape) != (b, l_pad):
+        raise ShapeMismatch("need exactly one scale per token row")
     dev = d_q.device
-    scores = torch.empty((n_q, b), dtype=torch.float64, device=dev)
-    argmax = torch.empty((n_q, b, l_q), dtype=torch.int32, device=dev) if want_argmax else None
-    rowmax = torch.empty((n_q, b, l_q), dtype=torch.float32, device=dev)
-    if valid_lens is not None:
-        valid_lens = valid_lens.to(device=dev, dtype=torch.int32).contiguous()
-    _lib.call("mxs_fused_score_int8", _dev.ptr(q_q.contiguous()), _dev.ptr(q_s.contiguous()), n_q, l_q,
-              _dev.ptr(d_q.contiguous()), _dev.ptr(d_s.contiguous()), b, l_pad, dim, _dev.ptr(valid_lens),
-              _dev.ptr(scores), _dev.ptr(argmax), _dev.ptr(rowmax), _dev.stream_handle(stream))
+    with _dev.on_device(d_q):
+        q_q, q_s, d_q, d_s = (t.contiguous() for t in (q_q, q_s, d_q, d_s))
+        if valid_lens is not None:
+            valid_lens = valid_lens.to(device=dev, dtype=torch.int32).contiguous()
+            if valid_lens.numel() != b:
+                raise ShapeMismatch(f"valid_lens holds {valid_lens.numel()} entries for {b} documents")
+            if validate:
+                _dev.validate_lens(valid_lens, l_pad, stream)
+        scores = torch.empty((n_q, b), dtype=torch.float64, device=dev)
+        argmax = torch.empty((n_q, b, l_q), dtype=torch.int32, device=dev) if want_argmax else None
+        rowmax = torch.empty((n_q, b, l_q), dtype=torch.float32, device=dev) if want_rowmax else None
+        for t in (q_q, q_s, d_q, d_s, valid_lens):
+            _dev.keep_alive(t, stream)
+        _lib.call("mxs_fused_score_int8", _dev.ptr(q_q), _dev.ptr(q_s), n_q, l_q, _dev.ptr(d_q), _dev.ptr(d_s), b, l_pad,
+                  dim, _dev.ptr(valid_lens), _dev.ptr(scores), _dev.ptr(argmax), _dev.ptr(rowmax),
+                  _dev.stream_handle(stream, dev))
     return scores, argmax, rowmax
 
 
@@ -166,7 +180,7 @@ def fused_score_int8(q_quant: QuantizedMatrix, d_quant: QuantizedMatrix, valid_l
     qm = q_quant if isinstance(q_quant, QuantizedMatrix) else QuantizedMatrix(q_quant.q, q_quant.scale)
     dm = d_quant if isinstance(d_quant, QuantizedMatrix) else QuantizedMatrix(d_quant.q, d_quant.scale)
     vl = torch.tensor([valid_len], dtype=torch.int32, device=dm.q.device)
-    scores, argmax, _ = score_int8(qm.q[None], qm.scale[None], dm.q[None], dm.scale[None], vl)
+    scores, argmax, _ = score_int8(qm.q[None], qm.scale[None], dm.q[None], dm.scale[None], vl, validate=False)
     rep.add_read(qm.q.numel() + qm.scale.numel() * 4)
     rep.add_read(dm.rows * (dm.dim + 4))
     rep.add_macs(2 * qm.rows * dm.rows * dm.dim)
@@ -196,7 +210,7 @@ def fused_score_int8_batch(q_quant, corpus, valid_lens=None, report: TrafficRepo
         if (lens_host < 1).any():
             raise EmptyDocument(int(np.argmax(lens_host < 1)))
         vl = torch.from_numpy(lens_host).to(corpus.q.device)
-    scores, argmax, _ = score_int8(qq, qs, corpus.q, corpus.scales, vl)
+    scores, argmax, _ = score_int8(qq, qs, corpus.q, corpus.scales, vl, validate=False)
     n_q, l_q, _ = qq.shape
     rep.add_read(n_q * l_q * (dim + 4))
     rep.add_read(n_q * b * l_pad * (dim + 4))
@@ -245,13 +259,13 @@ def two_stage_topk(query, corpus_q, corpus_full: DocBatch, k: int, shortlist_fac
     qm = query if isinstance(query, EmbeddingMatrix) else EmbeddingMatrix(query.data if hasattr(query, "rows") else query)
     qq, qs = quantize_tensor(qm.data)
     dq, ds, vl = _corpus_q_tensors(corpus_q)
-    coarse, _, _ = score_int8(qq[None], qs[None], dq, ds, vl, want_argmax=False)
+    coarse, _, _ = score_int8(qq[None], qs[None], dq, ds, vl, want_argmax=False, validate=False)
     shortlist_n = min(k * shortlist_factor, n_docs)
     _, short_ids = device_topk(coarse[0], shortlist_n)
     short_ids, _ = torch.sort(short_ids)  # shortlist positions in id order: ties rank by lower id
     D = corpus_full.data.index_select(0, short_ids)
     vls = corpus_full.valid_lens.index_select(0, short_ids)
-    fine, _, _ = score_dense(qm.data[None].to(D.dtype), D, vls, want_argmax=False)
+    fine, _, _ = score_dense(qm.data[None].to(D.dtype), D, vls, want_argmax=False, validate=False)
     top_s, top_pos = device_topk(fine[0], k)
     ids = short_ids.index_select(0, top_pos).cpu().tolist()
     rep.add_read(n_docs * dq.shape[1] * (dq.shape[2] + 4))

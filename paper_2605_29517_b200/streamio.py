@@ -348,7 +348,7 @@ def _stream(query, reader: CorpusReader, block_docs: int, k: int, report, comput
             data = raw if work_dtype == file_dtype else raw.to(work_dtype)
             if reader.layout == "packed":
                 cu = torch.from_numpy(rel).to(dev, non_blocking=True)
-                s, _, _ = score_varlen(q, data, cu, want_argmax=False, exact=exact)
+                s, _, _ = score_varlen(q, data, cu, want_argmax=False, exact=exact, validate=False)
             else:
                 s, _, _ = score_dense(q, data, exact=exact, want_argmax=False)
             rep.add_read(nbytes)
@@ -427,7 +427,8 @@ def stream_score_host(query, docs_host: torch.Tensor, k: int, block_docs: int = 
         data = devb[slot][:count]
         if work_dtype != data.dtype:
             data = data.to(work_dtype)
-        s, _, _ = score_dense(q, data, None if vl is None else vl[first:first + count], want_argmax=False)
+        s, _, _ = score_dense(q, data, None if vl is None else vl[first:first + count], want_argmax=False,
+                              validate=False)
         if scores is not None:
             scores[first:first + count].copy_(s[0])
         bs, bi = topk(s[0], min(k, count), id_offset=first)

@@ -1,0 +1,320 @@
+"""north_star acceptance criteria asserted AT their own configs (BASELINE.json configs[1..4]).
+
+* C2  ColPali rerank, 10K docs x 1024 x 1024 x 128, bf16: every score within 1e-3 relative of a
+      float64 oracle over the full corpus (dense f64 on the device), 32
+      sampled documents against the C fp32 oracle (scores + argmax on clear rows), and 100 %
+      top-20 agreement on a 10K-document planted corpus.
+* C3  in-batch 64 x 64 at the ColPali shape: the forward against the f64 oracle (all pairs) and
+      the C fp32 oracle (sampled pairs).
+* C4  INT8 x INT8 at the C2 shape, 10K docs: 32 sampled documents bit-exact (scores and argmax,
+      ties included) against the C INT8 oracle; Spearman >= 0.99 and identical top-20 against
+      the BF16 path on the full planted corpus (maxsim/quant.py:171-179, tests/test_quant.py:84-95,
+      tests/test_acceptance.py:327-358).
+* C5  varlen 1M-document ColBERT corpus (L_d in [32, 512], L_q = 32): >= 1000 sampled documents,
+      concentrated around token-balanced shard boundaries, against the C oracle; shard-wise
+      scoring bit-identical to the single launch.
+* Float argmax: exact on every row whose oracle top-2 gap exceeds 1e-5 (Appendix A.2); the
+  excluded-row count is printed.
+
+Inputs are generated on the device (seeded torch generators) because the host would need
+5-70 GB for them; the oracle sees exactly the values the kernels see.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_29517_b200 as mx
+from oracle import oracle as orc
+from paper_2605_29517_b200.parallel import shard_bounds
+from paper_2605_29517_b200.quant import quantize_tensor
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-3
+GAP = 1e-5
+
+
+def unit_rows(g, shape, dtype=torch.bfloat16):
+    x = torch.randn(*shape, device="cuda", generator=g, dtype=torch.float32)
+    return (x / x.norm(dim=-1, keepdim=True)).to(dtype)
+
+
+def f64_oracle(Q, D, valid_lens=None, chunk=32):
+    """Dense float64 MaxSim on the device (maxsim/reference.py:76-120 in f64), chunked over docs.
+
+    Q [n_q, l_q, d], D [B, L, d] (any float dtype; widened exactly).  Returns (scores f64 [n_q, B],
+    argmax int64 [n_q, B, l_q], top-2 gap f64 [n_q, B, l_q])."""
+    n_q, l_q, d = Q.shape
+    b, L, _ = D.shape
+    Qd = Q.double()
+    scores = torch.empty(n_q, b, dtype=torch.float64, device="cuda")
+    arg = torch.empty(n_q, b, l_q, dtype=torch.int64, device="cuda")
+    gap = torch.empty(n_q, b, l_q, dtype=torch.float64, device="cuda")
+    cols = torch.arange(L, device="cuda")
+    for lo in range(0, b, chunk):
+        hi = min(b, lo + chunk)
+        S = torch.einsum("qid,bjd->qbij", Qd, D[lo:hi].double())
+        if valid_lens is not None:
+            mask = cols[None, None, None, :] >= valid_lens[lo:hi].to("cuda")[None, :, None, None]
+            S = S.masked_fill(mask, float("-inf"))
+        top = torch.topk(S, min(2, L), dim=-1)
+        scores[:, lo:hi] = top.values[..., 0].sum(dim=-1)
+        arg[:, lo:hi] = top.indices[..., 0]
+        g = (top.values[..., 0] - top.values[..., 1]) if L > 1 else torch.full_like(top.values[..., 0], float("inf"))
+        gap[:, lo:hi] = torch.nan_to_num(g, nan=float("inf"), posinf=float("inf"))
+        del S, top
+    return scores, arg, gap
+
+
+def ranked(scores_1d, k):
+    """Reference ranking (score desc, id asc) of a 1-D score vector: first k ids."""
+    s = np.asarray(scores_1d, np.float64)
+    return list(np.lexsort((np.arange(s.size), -s))[:k])
+
+
+def planted_device(g, q, n_docs, len_d, cos_of_doc):
+    """Planted corpus on the device (maxsim/synth.py:70-106 construction): token i of document b is
+    cos_b * q_unit[i] + sin_b * (random unit vector orthogonal to q_unit[i]); the rest are random
+    unit tokens.  cos_of_doc: float64 [n_docs].  Returns fp32 [n_docs, len_d, d]."""
+    l_q, d = q.shape
+    qu = q.double() / q.double().norm(dim=-1, keepdim=True)
+    out = torch.empty(n_docs, len_d, d, dtype=torch.float32, device="cuda")
+    m = min(l_q, len_d)
+    for lo in range(0, n_docs, 256):
+        hi = min(n_docs, lo + 256)
+        t = torch.randn(hi - lo, len_d, d, device="cuda", generator=g, dtype=torch.float64)
+        t = t / t.norm(dim=-1, keepdim=True)
+        perp = torch.randn(hi - lo, m, d, device="cuda", generator=g, dtype=torch.float64)
+        base = qu[:m][None]
+        perp = perp - (perp * base).sum(-1, keepdim=True) * base
+        perp = perp / perp.norm(dim=-1, keepdim=True)
+        c = cos_of_doc[lo:hi].to("cuda")[:, None, None]
+        t[:, :m] = c * base + torch.sqrt(1.0 - c * c) * perp
+        out[lo:hi] = t.float()
+    return out
+
+
+def spearman(a, b):
+    ra = np.argsort(np.argsort(np.asarray(a))).astype(np.float64)
+    rb = np.argsort(np.argsort(np.asarray(b))).astype(np.float64)
+    ra -= ra.mean()
+    rb -= rb.mean()
+    return float((ra * rb).sum() / np.sqrt((ra * ra).sum() * (rb * rb).sum()))
+
+
+def assert_scores_rel(got, ref, what):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert float(rel.max()) < REL, f"{what}: worst relative error {rel.max():.3e}"
+    return float(rel.max())
+
+
+def assert_argmax_clear(got, ref, gap, what):
+    safe = gap > GAP
+    n_ex = int((~safe).sum())
+    bad = int((got[safe] != ref[safe]).sum())
+    print(f"{what}: argmax compared on {int(safe.sum())} rows, {n_ex} excluded (top-2 gap <= {GAP}), {bad} differ")
+    assert bad == 0, f"{what}: {bad} argmax mismatches on clear rows"
+    assert safe.mean() > 0.99
+    return n_ex
+
+
+# ------------------------------------------------------------------ C2
+@pytest.fixture(scope="module")
+def c2():
+    g = torch.Generator(device="cuda").manual_seed(2026)
+    Q = unit_rows(g, (1, 1024, 128))
+    D = unit_rows(g, (10_000, 1024, 128))
+    return Q, D
+
+
+def test_c2_full_corpus_scores_and_argmax_vs_f64(c2):
+    Q, D = c2
+    sc, am, _ = mx.score_dense(Q, D)
+    sr, _, _ = mx.score_dense(Q, D, want_argmax=False)
+    assert torch.equal(sc, sr), "rerank mode must give the argmax mode's score bits"
+    ref_s, ref_a, gap = f64_oracle(Q, D)
+    worst = assert_scores_rel(sc.cpu().numpy(), ref_s.cpu().numpy(), "C2 10K scores vs f64")
+    print(f"C2 10K: worst relative error {worst:.2e}")
+    assert_argmax_clear(am.long().cpu().numpy(), ref_a.cpu().numpy(), gap.cpu().numpy(), "C2 10K")
+
+
+def test_c2_sampled_docs_vs_c_oracle(c2):
+    Q, D = c2
+    sc, am, _ = mx.score_dense(Q, D)
+    idx = torch.tensor(sorted(set(np.random.default_rng(5).choice(10_000, 30, replace=False).tolist()) | {0, 9999}),
+                       device="cuda")
+    assert idx.numel() >= 32
+    Qo = Q.float().cpu().numpy()
+    Do = D.index_select(0, idx).float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_batch(Qo, Do)
+    assert_scores_rel(sc[:, idx].cpu().numpy(), ref_s, "C2 sampled vs fp32 oracle")
+    _, _, gap = f64_oracle(Q, D.index_select(0, idx))
+    assert_argmax_clear(am[:, idx].cpu().numpy(), ref_a, gap.cpu().numpy(), "C2 sampled vs fp32 oracle")
+
+
+@pytest.fixture(scope="module")
+def planted10k():
+    """10K-doc planted corpus at the ColPali shape: 20 documents with clearly higher planted
+    similarity (cos 0.95 .. 0.90) at random ids, the rest spread over 0.85 .. 0.70 -- no
+    near-ties at the rank-20 boundary (maxsim/synth.py:80-88)."""
+    g = torch.Generator(device="cuda").manual_seed(77)
+    q = unit_rows(g, (1024, 128), torch.float32)
+    n = 10_000
+    cos = torch.cat([torch.linspace(0.95, 0.90, 20, dtype=torch.float64),
+                     torch.linspace(0.85, 0.70, n - 20, dtype=torch.float64)])
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(78))
+    D = planted_device(g, q, n, 1024, cos[perm])
+    return q, D, perm
+
+
+def test_c2_top20_planted_10k(planted10k):
+    q, D32, _ = planted10k
+    Q = q[None].bfloat16()
+    D = D32.bfloat16()
+    sc, _, _ = mx.score_dense(Q, D, want_argmax=False)
+    ref_s, _, _ = f64_oracle(Q, D)
+    assert_scores_rel(sc.cpu().numpy(), ref_s.cpu().numpy(), "C2 planted scores vs f64")
+    top_gpu = ranked(sc[0].cpu().numpy(), 20)
+    top_ref = ranked(ref_s[0].cpu().numpy(), 20)
+    assert top_gpu == top_ref
+    # the device top-K (K9) returns the same ordered list
+    _, ids = mx.topk(sc[0], 20)
+    assert ids.cpu().tolist() == top_ref
+    # and the fp32 C oracle agrees on the top-20 documents' scores
+    sel = torch.tensor(top_ref, device="cuda")
+    o_s, _ = orc.fused_score_batch(Q.float().cpu().numpy(), D.index_select(0, sel).float().cpu().numpy())
+    assert_scores_rel(sc[:, sel].cpu().numpy(), o_s, "C2 planted top-20 vs fp32 oracle")
+
+
+# ------------------------------------------------------------------ C4
+def test_c4_int8_sampled_bitexact_10k(c2):
+    Q, D = c2
+    qq, qs = quantize_tensor(Q.float())
+    dq, ds = quantize_tensor(D)
+    s8, a8, _ = mx.score_int8(qq, qs, dq, ds)
+    s8r, _, _ = mx.score_int8(qq, qs, dq, ds, want_argmax=False)
+    assert torch.equal(s8, s8r), "INT8 rerank kernel must give the argmax kernel's score bits"
+    idx = np.array(sorted(set(np.random.default_rng(6).choice(10_000, 30, replace=False).tolist()) | {0, 9999}))
+    it = torch.from_numpy(idx).cuda()
+    ref_s, ref_a = orc.fused_score_int8(qq.cpu().numpy(), qs.cpu().numpy(), dq.index_select(0, it).cpu().numpy(),
+                                        ds.index_select(0, it).cpu().numpy())
+    assert np.array_equal(s8[:, it].cpu().numpy(), ref_s), "INT8 scores not bit-identical"
+    assert np.array_equal(a8[:, it].cpu().numpy(), ref_a), "INT8 argmax not bit-identical"
+    print(f"C4: {idx.size} sampled docs bit-exact (scores and argmax incl. ties)")
+
+
+def test_c4_int8_fidelity_vs_bf16_planted_10k(planted10k):
+    q, D32, _ = planted10k
+    Q = q[None]
+    qq, qs = quantize_tensor(Q)
+    dq, ds = quantize_tensor(D32)
+    s8, _, _ = mx.score_int8(qq, qs, dq, ds, want_argmax=False)
+    sb, _, _ = mx.score_dense(Q.bfloat16(), D32.bfloat16(), want_argmax=False)
+    rho = spearman(s8[0].cpu().numpy(), sb[0].cpu().numpy())
+    print(f"C4 planted 10K: Spearman(INT8, BF16) = {rho:.6f}")
+    assert rho >= 0.99
+    assert set(ranked(s8[0].cpu().numpy(), 20)) == set(ranked(sb[0].cpu().numpy(), 20))
+    # 32 sampled planted documents bit-exact against the INT8 oracle as well
+    it = torch.arange(0, 10_000, 313, device="cuda")[:32]
+    ref_s, _ = orc.fused_score_int8(qq.cpu().numpy(), qs.cpu().numpy(), dq.index_select(0, it).cpu().numpy(),
+                                    ds.index_select(0, it).cpu().numpy())
+    assert np.array_equal(s8[:, it].cpu().numpy(), ref_s)
+
+
+# ------------------------------------------------------------------ C3
+def test_c3_inbatch_forward_vs_oracle():
+    g = torch.Generator(device="cuda").manual_seed(33)
+    Q = unit_rows(g, (64, 1024, 128))
+    D = unit_rows(g, (64, 1024, 128))
+    sc, am, _ = mx.score_dense(Q, D)
+    ref_s, ref_a, gap = f64_oracle(Q, D, chunk=4)
+    assert_scores_rel(sc.cpu().numpy(), ref_s.cpu().numpy(), "C3 64x64 vs f64")
+    assert_argmax_clear(am.long().cpu().numpy(), ref_a.cpu().numpy(), gap.cpu().numpy(), "C3 64x64")
+    # sampled pairs against the C fp32 oracle (diagonal + off-diagonal)
+    qi, bi = [0, 17, 63], [0, 40, 63]
+    o_s, o_a = orc.fused_score_batch(Q[qi].float().cpu().numpy(), D[bi].float().cpu().numpy())
+    assert_scores_rel(sc[qi][:, bi].cpu().numpy(), o_s, "C3 sampled vs fp32 oracle")
+    sub_gap = gap[qi][:, bi].cpu().numpy()
+    assert_argmax_clear(am[qi][:, bi].cpu().numpy(), o_a, sub_gap, "C3 sampled vs fp32 oracle")
+
+
+# ------------------------------------------------------------------ varlen (C5)
+def varlen_oracle_gap(Qo, toks, cu):
+    """float64 top-2 gap per (q, doc, row) of a packed corpus (host, small)."""
+    n_q, l_q, _ = Qo.shape
+    b = cu.size - 1
+    gap = np.full((n_q, b, l_q), np.inf)
+    Q64 = Qo.astype(np.float64)
+    for d in range(b):
+        S = np.einsum("qid,jd->qij", Q64, toks[cu[d]:cu[d + 1]].astype(np.float64))
+        if S.shape[-1] > 1:
+            part = np.sort(S, axis=-1)
+            gap[:, d] = part[..., -1] - part[..., -2]
+    return gap
+
+
+@pytest.mark.parametrize("n_docs,lo,hi,l_q,n_q", [(2000, 32, 512, 32, 1), (3000, 1, 300, 32, 1), (500, 1, 300, 16, 4),
+                                                 (300, 5, 700, 128, 1), (40, 50, 700, 1024, 1)])
+def test_varlen_tensor_core_argmax_exact_on_clear_rows(n_docs, lo, hi, l_q, n_q):
+    """K5 argmax equals the oracle's on EVERY row whose top-2 gap exceeds 1e-5; documents
+    straddle 128-token tiles and 32-token scan ranges; scores within 1e-3; fused S4 path (l_q | 32)
+    and the rowmax + rowsum path (l_q = 128, 1024) both covered."""
+    rng = np.random.default_rng(n_docs * 7 + l_q)
+    lens = rng.integers(lo, hi + 1, n_docs)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    toks = torch.from_numpy(np.concatenate(orc.make_corpus(n_docs, lens, 128, seed=int(rng.integers(1 << 30))))).cuda()
+    toks = toks.bfloat16()
+    Q = torch.from_numpy(orc.make_queries(n_q, l_q, 128, seed=int(rng.integers(1 << 30)))).cuda().bfloat16()
+    s_tc, a_tc, _ = mx.score_varlen(Q, toks, torch.from_numpy(cu).cuda())
+    Qo, To = Q.float().cpu().numpy(), toks.float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_varlen(Qo, To, cu)
+    assert_scores_rel(s_tc.cpu().numpy(), ref_s, "varlen scores")
+    assert_argmax_clear(a_tc.cpu().numpy(), ref_a, varlen_oracle_gap(Qo, To, cu), f"varlen n={n_docs} l_q={l_q}")
+    # rowmax opt-in output gives the same scores (rowsum pass) as the fused epilogue sum
+    s_rm, _, rm = mx.score_varlen(Q, toks, torch.from_numpy(cu).cuda(), want_argmax=False, want_rowmax=True)
+    assert rm is not None and torch.equal(s_rm, s_tc)
+
+
+def test_c5_1m_docs_sampled_vs_oracle_and_shard_invariance():
+    """configs[4] at full size: 1M documents, L_d ~ U[32, 512] (mean 272, 69.7 GB bf16), L_q = 32."""
+    n = 1_000_000
+    lens = np.random.default_rng(5).integers(32, 513, n)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    T = int(cu[-1])
+    g = torch.Generator(device="cuda").manual_seed(55)
+    toks = torch.empty(T, 128, dtype=torch.bfloat16, device="cuda")
+    step = 1 << 24
+    for lo in range(0, T, step):
+        hi = min(T, lo + step)
+        toks[lo:hi] = unit_rows(g, (hi - lo, 128))
+    Q = unit_rows(g, (1, 32, 128))
+    cu_d = torch.from_numpy(cu).cuda()
+    sc, am, _ = mx.score_varlen(Q, toks, cu_d)
+    torch.cuda.synchronize()
+    # token-balanced 8-way shards: each shard scored on its own gives the same bits
+    bounds = [shard_bounds(n, 8, r, lens) for r in range(8)]
+    for r, (a, b) in enumerate(bounds):
+        cs = torch.from_numpy(cu[a:b + 1] - cu[a]).cuda()
+        s_r, a_r, _ = mx.score_varlen(Q, toks[int(cu[a]):int(cu[b])], cs)
+        assert torch.equal(s_r, sc[:, a:b]), f"shard {r} scores differ"
+        assert torch.equal(a_r, am[:, a:b]), f"shard {r} argmax differs"
+    # >= 1000 sampled documents: 24 around every shard boundary + random ones, vs the oracle
+    rng = np.random.default_rng(9)
+    pick = set(rng.choice(n, 800, replace=False).tolist())
+    for a, _ in bounds:
+        pick |= set(range(max(0, a - 12), min(n, a + 12)))
+    pick |= {0, n - 1}
+    idx = np.array(sorted(pick))
+    assert idx.size >= 1000
+    sub_cu = np.concatenate([[0], np.cumsum(lens[idx])]).astype(np.int64)
+    rows = np.concatenate([np.arange(cu[i], cu[i + 1]) for i in idx])
+    sub = toks.index_select(0, torch.from_numpy(rows).cuda()).float().cpu().numpy()
+    Qo = Q.float().cpu().numpy()
+    ref_s, ref_a = orc.fused_score_varlen(Qo, sub, sub_cu)
+    it = torch.from_numpy(idx).cuda()
+    assert_scores_rel(sc[:, it].cpu().numpy(), ref_s, "C5 1M sampled scores")
+    assert_argmax_clear(am[:, it].cpu().numpy(), ref_a, varlen_oracle_gap(Qo, sub, sub_cu), "C5 1M sampled")
+    print(f"C5 1M: {idx.size} sampled docs (incl. 8 shard boundaries) vs oracle, shards bit-identical")

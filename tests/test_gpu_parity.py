@@ -43,6 +43,19 @@ def top2_gap(Q, D, valid_lens):
     return np.where(np.isfinite(gap), gap, np.inf)
 
 
+def varlen_top2_gap(Q, toks, cu):
+    """float64 top-2 gap per (q, document, query row) of a packed corpus."""
+    n_q, l_q, _ = Q.shape
+    gap = np.full((n_q, cu.size - 1, l_q), np.inf)
+    Q64 = Q.astype(np.float64)
+    for d in range(cu.size - 1):
+        S = np.einsum("qid,jd->qij", Q64, toks[cu[d]:cu[d + 1]].astype(np.float64))
+        if S.shape[-1] > 1:
+            part = np.sort(S, axis=-1)
+            gap[:, d] = part[..., -1] - part[..., -2]
+    return gap
+
+
 @pytest.mark.parametrize("dim", [8, 16, 40, 200, 320, 512])
 def test_forward_unusual_dims(dim):
     """Embedding widths off the 64-element atom (zero-filled K tail in TMA / TMEM) and past the
@@ -177,8 +190,8 @@ def test_c2_scale_sampled_parity():
     safe = top2_gap(Qo, Do, [1024] * len(idx)) > GAP
     assert np.array_equal(am[:, idx].cpu().numpy()[safe], ref_a[safe])
     # the two Q row groups of one document are independent: splitting the query agrees exactly
-    s_lo, a_lo, r_lo = mx.score_dense(Q[:, :512].contiguous(), D[:100])
-    _, _, r_full = mx.score_dense(Q, D[:100])
+    s_lo, a_lo, r_lo = mx.score_dense(Q[:, :512].contiguous(), D[:100], want_rowmax=True)
+    _, _, r_full = mx.score_dense(Q, D[:100], want_rowmax=True)
     assert torch.equal(r_full[:, :, :512], r_lo)
 
 
@@ -318,8 +331,11 @@ def test_varlen_equals_padded_bf16():
     s_p, a_p, _ = mx.score_dense(cuda(q, torch.bfloat16), cuda(D, torch.bfloat16), cuda(vl))
     ref_s, ref_a = orc.fused_score_varlen(cuda(q, torch.bfloat16).float().cpu().numpy(), toks.float().cpu().numpy(), cu)
     assert rel_err(s_v.cpu().numpy(), ref_s) < REL and rel_err(s_p.cpu().numpy(), ref_s) < REL
-    agree = (a_v.cpu().numpy() == ref_a).mean()
-    assert agree > 0.999
+    # argmax: exact on every row whose oracle top-2 gap exceeds 1e-5
+    safe = varlen_top2_gap(cuda(q, torch.bfloat16).float().cpu().numpy(), toks.float().cpu().numpy(), cu) > GAP
+    assert safe.mean() > 0.99
+    assert np.array_equal(a_v.cpu().numpy()[safe], ref_a[safe])
+    assert np.array_equal(a_p.cpu().numpy()[safe], ref_a[safe])
 
 
 # ------------------------------------------------------------------ backward (K6, K7, K8)
@@ -575,4 +591,7 @@ def test_varlen_tensor_core_vs_exact_and_oracle(n_docs, lo, hi, l_q, n_q):
     ref_s, ref_a = orc.fused_score_varlen(Q.float().cpu().numpy(), toks.float().cpu().numpy(), cu)
     assert np.array_equal(s_ex.cpu().numpy(), ref_s) and np.array_equal(a_ex.cpu().numpy(), ref_a)
     assert rel_err(s_tc.cpu().numpy(), ref_s) < REL
-    assert (a_tc.cpu().numpy() == ref_a).mean() > 0.998
+    safe = varlen_top2_gap(Q.float().cpu().numpy(), toks.float().cpu().numpy(), cu) > GAP
+    print(f"varlen: {int((~safe).sum())} of {safe.size} rows excluded (top-2 gap <= {GAP})")
+    assert safe.mean() > 0.98
+    assert np.array_equal(a_tc.cpu().numpy()[safe], ref_a[safe])
