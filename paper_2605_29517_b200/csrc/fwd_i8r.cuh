@@ -15,7 +15,12 @@
 //     consumes its own slot in order (no mbarrier phase aliasing);
 //   * each set keeps, per Q block, a partial maximum over the tiles it happened to drain; at the
 //     end of a document the three partials of every row are max-combined through shared memory
-//     (double-buffered by document parity) and written once.
+//     (double-buffered by document parity) and written once;
+//   * fused S4 score: the combiner of each quadrant stores the combined maxima straight into
+//     cluster rank 0's row buffer (DSMEM) and arrives there; rank 0's score warp folds them.
+//     (Unlike fwd_ts, only 4 combiner warps per CTA and document pay the cluster-scope
+//     release; the CTA-local variant with per-rank score warps made ptxas spill in this
+//     register-capped kernel.)
 // Everything else (TS MMA with Q resident in TMEM, cluster multicast of document tiles,
 // TMA-staged INT8 scales, magic-number s32 -> f32) is fwd_ts.cuh's.
 #pragma once
@@ -42,8 +47,8 @@ struct R8SmemHeader {
   uint64_t qempty;
   uint64_t sfull[kScaleSlots];
   uint64_t sempty[kScaleSlots];
-  uint64_t sready[2];  // fused score row buffers (rank 0), see fwd_ts.cuh
-  uint64_t sfree[2];
+  uint64_t sready[2];  // fused score: the combiners of every CTA stored document n's maxima in rank 0's buffer [n & 1]
+  uint64_t sfree[2];   // fused score: rank 0's score warp consumed buffer [n & 1]
   uint32_t tmem_base;
   uint32_t pad;
 };
@@ -248,11 +253,11 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         int q, g, b;
         decode(u, q, g, b);
         const uint32_t sb = n & 1u;
-        mbar_wait_cl<CL>(&hdr->sready[sb], (n >> 1) & 1u);
+        mbar_wait_cl_idle<CL>(&hdr->sready[sb], (n >> 1) & 1u);
         const double sc = warp_score_sum(sSum + sb * p.sum_rows, p.l_q);
         if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
         __syncwarp();
-        if (lane < (uint32_t)CL) mbar_arrive_rank<CL>(&hdr->sfree[sb], lane);
+        if (lane < (uint32_t)CL) mbar_arrive_rank<CL>(&hdr->sfree[sb], lane);  // release: buffer reusable
       }
     }
   } else {

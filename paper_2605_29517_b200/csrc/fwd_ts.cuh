@@ -14,10 +14,11 @@
 //     final max is resolved once per (row, document) from that copy -- no per-chunk rescans
 //     across the warp.
 //   * fused S4 score: at the end of a document every epilogue thread stores its row maxima into a
-//     double-buffered row array in the shared memory of cluster rank 0 (DSMEM stores for the
-//     other ranks) and arrives on that buffer's mbarrier; a dedicated score warp of rank 0 folds
-//     the L_q maxima with the certified f64 sum (score_sum.cuh) and writes the score, so the
-//     [N_q, B, L_q] row maxima never reach HBM (they are written only on request).
+//     double-buffered row array in its OWN shared memory and arrives on a CTA-local mbarrier (no
+//     cluster-scope operation on the epilogue's critical path).  A score warp per CTA forwards
+//     readiness to cluster rank 0, whose score warp reads the other ranks' rows through DSMEM,
+//     folds the L_q maxima with the certified f64 sum (score_sum.cuh) and writes the score, so
+//     the [N_q, B, L_q] row maxima never reach HBM (they are written only on request).
 #pragma once
 #include "fwd_tc.cuh"
 #include "score_sum.cuh"
@@ -40,8 +41,10 @@ struct TsSmemHeader {
   uint64_t qempty;
   uint64_t sfull[kScaleSlots];   // INT8 scale ring: TMA bulk copy landed
   uint64_t sempty[kScaleSlots];  // INT8 scale ring: all 8 epilogue warps done with the tile
-  uint64_t sready[2];            // fused score: a document's row maxima are in row buffer [doc & 1] (rank 0)
-  uint64_t sfree[2];             // fused score: rank 0's score warp has consumed row buffer [doc & 1]
+  uint64_t sready[2];            // fused score: this CTA's row maxima of document n are in row buffer [n & 1]
+  uint64_t sfree[2];             // fused score: row buffer [n & 1] may be refilled (local score warp)
+  uint64_t speer[2];             // fused score, rank 0: the other ranks' buffers [n & 1] are ready
+  uint64_t sdone[2];             // fused score, rank != 0: rank 0 has read buffer [n & 1]
   uint32_t tmem_base;
   uint32_t pad;
 };
@@ -212,6 +215,44 @@ MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m
   }
 }
 
+// Score warp of the fused S4 epilogue (fwd_ts_kernel, fwd_i8r_kernel).  The CTA's producers store
+// the row maxima of document n into row buffer [n & 1] of their OWN shared memory and arrive on
+// sready[n & 1] (CTA scope) -- nothing cluster-wide on the epilogue's critical path.  The score
+// warp of rank r != 0 copies its rows into rank 0's buffer through DSMEM (once rank 0 has
+// consumed that buffer's previous document: sdone) and arrives on rank 0's speer (release,
+// cluster scope); the score warp of rank 0 then holds all L_q maxima locally, computes the
+// certified f64 sum and writes the score.  sfree[n & 1] re-arms a CTA's own buffer.
+template <int CL, typename Decode>
+MXS_DEV void fused_score_warp(const FwdTcParams& p, uint64_t* sready, uint64_t* sfree, uint64_t* speer,
+                              uint64_t* sdone, float* sSum, long long u_begin, long long u_end, Decode decode,
+                              int crank, uint32_t lane) {
+  uint32_t n = 0;
+  for (long long u = u_begin; u < u_end; ++u, ++n) {
+    const uint32_t sb = n & 1u, ph = (n >> 1) & 1u;
+    float* buf = sSum + sb * p.sum_rows;
+    mbar_wait_idle(&sready[sb], ph);  // this CTA's rows are in
+    if (crank == 0) {
+      int q, g, b;
+      decode(u, q, g, b);
+      if constexpr (CL > 1) mbar_wait_cluster_idle(&speer[sb], ph);  // and every other rank's
+      const double sc = warp_score_sum(buf, p.l_q);
+      if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[sb]);
+      if constexpr (CL > 1) {  // release: rank `lane` may refill our buffer [sb]
+        if (lane >= 1 && lane < (uint32_t)CL) mbar_arrive_cluster(mapa_u32(smem_u32(&sdone[sb]), lane));
+      }
+    } else if constexpr (CL > 1) {
+      mbar_wait_cluster_idle(&sdone[sb], ph ^ 1u);  // rank 0 consumed its buffer [sb] two documents ago
+      const int r0 = crank * p.qb * kTileRows, r1 = min(p.l_q, r0 + p.qb * kTileRows);
+      for (int i = r0 + (int)lane; i < r1; i += 32) st_cluster_f32(mapa_u32(smem_u32(buf + i), 0u), buf[i]);
+      mbar_arrive_cluster(mapa_u32(smem_u32(&speer[sb]), 0u));  // every lane: release of its own stores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[sb]);
+    }
+  }
+}
+
 template <TcKind KIND, int KA, int CL>
 __global__ void __launch_bounds__(kTsThreads, 1)
     fwd_ts_kernel(const __grid_constant__ CUtensorMap tmD, const FwdTcParams p) {
@@ -273,8 +314,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       mbar_init(&hdr->sempty[s], kEpiWarps);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&hdr->sready[s], 32 * kEpiWarps * CL);  // every epilogue lane of the cluster
+      mbar_init(&hdr->sready[s], 32 * kEpiWarps);  // every epilogue lane of this CTA
       mbar_init(&hdr->sfree[s], 1);
+      mbar_init(&hdr->speer[s], CL > 1 ? 32 * (CL - 1) : 1);
+      mbar_init(&hdr->sdone[s], 1);
     }
     fence_mbar_init();
   }
@@ -413,20 +456,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       mbar_wait(&hdr->qempty, qphase ^ 1u);
     }
   } else if (warp == kTsSumWarp) {
-    // ------------------------------------------------------------------ fused S4 score (rank 0)
-    if (fuse && crank == 0) {
-      uint32_t n = 0;
-      for (long long u = u_begin; u < u_end; ++u, ++n) {
-        int q, g, b;
-        decode(u, q, g, b);
-        const uint32_t sb = n & 1u;
-        mbar_wait_cl<CL>(&hdr->sready[sb], (n >> 1) & 1u);
-        const double sc = warp_score_sum(sSum + sb * p.sum_rows, p.l_q);
-        if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
-        __syncwarp();
-        if (lane < (uint32_t)CL) mbar_arrive_rank<CL>(&hdr->sfree[sb], lane);
-      }
-    }
+    // ------------------------------------------------------------------ fused S4 score
+    if (fuse) fused_score_warp<CL>(p, hdr->sready, hdr->sfree, hdr->speer, hdr->sdone, sSum, u_begin, u_end, decode,
+                                   crank, lane);
   } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
     // warp w in [2, 10): TMEM lane quadrant w % 4 (hardware rule), set (w - 2) / 4.
@@ -603,6 +635,19 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           ++sc_n;
         }
       }
+      if (fuse) {  // row maxima -> this CTA's row buffer, then every lane arrives (CTA scope)
+        const uint32_t sb = ndoc & 1u;
+        mbar_wait(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
+        float* dst = sSum + sb * p.sum_rows;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int mb = 2 * i + wset;
+          const int row = (g * p.qb + mb) * kTileRows + row_local;
+          if (mb < qbv && row < p.l_q) dst[row] = m[i];
+        }
+        mbar_arrive(&hdr->sready[sb]);
+        ++ndoc;
+      }
       const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -617,19 +662,6 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             p.argmax[obase + row] = ntiles ? cb[i] + first_argmax32_chain(w, m[i]) : 0;  // 0: empty (invalid) doc
           }
         }
-      }
-      if (fuse) {  // row maxima -> rank 0's row buffer, then every lane arrives (release, cluster scope)
-        const uint32_t sb = ndoc & 1u;
-        mbar_wait_cl<CL>(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
-        float* dst = sSum + sb * p.sum_rows;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int mb = 2 * i + wset;
-          const int row = (g * p.qb + mb) * kTileRows + row_local;
-          if (mb < qbv && row < p.l_q) st_rank0_f32<CL>(dst + row, m[i]);
-        }
-        mbar_arrive_rank<CL>(&hdr->sready[sb], 0u);
-        ++ndoc;
       }
     }
   }

@@ -29,7 +29,7 @@ int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   const int cl = (n_groups == 2 || n_groups == 4) ? n_groups : 1;
   const size_t max_smem = 232448 - sizeof(mxs::R8SmemHeader);
   const int dbg = env_int("MXS_DEBUG", 0);  // 2: slots released unread; 3 (bf16/fp16): no drain wait
-  const bool fuse = scores != nullptr && cl == n_groups && !(!kI8 && dbg == 3);
+  const bool fuse = scores != nullptr && cl == n_groups && !(!kI8 && dbg == 3) && env_int("MXS_FWD_FUSE", 1) != 0;
   if (!fuse && !rowmax) return MXS_UNSUPPORTED;
   const int sum_rows = fuse ? nmb * 128 : 0;
   const size_t fixed = mxs::fwd_i8r_smem_bytes(ka, 0, kI8, sum_rows);

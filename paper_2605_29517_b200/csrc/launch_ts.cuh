@@ -31,7 +31,8 @@ int launch_fwd_ts(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_
   // fused S4 sum when one cluster holds a whole query (every Q row group of it) and the profiling
   // knob MXS_DEBUG=3 (no drain) is off
   const int dbg = env_int("MXS_DEBUG", 0);
-  const bool fuse = scores != nullptr && cl == n_groups && !(KIND != mxs::TcKind::I8 && dbg == 3);
+  const bool fuse = scores != nullptr && cl == n_groups && !(KIND != mxs::TcKind::I8 && dbg == 3) &&
+                    env_int("MXS_FWD_FUSE", 1) != 0;
   if (!fuse && !rowmax) return MXS_UNSUPPORTED;  // the caller supplies row maxima for the rowsum pass
   const int sum_rows = fuse ? nmb * 128 : 0;
   const size_t fixed = mxs::fwd_ts_smem_bytes(0, qb, 0, scale_ring, bias, argmax != nullptr, sum_rows);

@@ -15,26 +15,27 @@ int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens
                      int64_t n_tokens, int64_t dim, float* rowmax, int32_t* argmax, double* scores, int* fused,
                      cudaStream_t st) {
   *fused = 0;
-  // fused S4 score when a query's rows fit one warp's aligned lane segment (l_q divides 32)
-  const bool fuse = scores != nullptr && l_q <= 32 && (32 % l_q) == 0;
-  if (!fuse && !rowmax) return MXS_UNSUPPORTED;
   static_assert(KIND != mxs::TcKind::I8, "varlen is a bf16 / f16 path");
   const int eb = 2;
   const long long rows = n_q * l_q;
+  // fused S4 score when a query's rows fit one warp's aligned lane segment (l_q divides 32)
+  // (one launch of <= 32 rows: the fused kernel is compiled for the 4-copy layout only)
+  const bool fuse = scores != nullptr && l_q <= 32 && (32 % l_q) == 0 && rows <= 32 && env_int("MXS_VARLEN_FUSE", 1) != 0;
+  if (!fuse && !rowmax) return MXS_UNSUPPORTED;
   if ((dim * eb) % 16 != 0 || rows >= (1LL << 31)) return MXS_UNSUPPORTED;
   const int ka = (int)((dim * eb + 127) / 128);
   if (ka > 4) return MXS_UNSUPPORTED;
-  const size_t max_smem = 232448 - sizeof(mxs::VrSmemHeader);
+  const size_t max_smem = 232448 - sizeof(mxs::VrSmemHeader) - (fuse ? sizeof(mxs::VrRing) : 0);
   const size_t fixed = mxs::varlen_rows_smem_bytes(ka, 0);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kAtomBytes));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
   void (*kern)(const CUtensorMap, const CUtensorMap, const mxs::VarlenRowsParams) = nullptr;
   switch (ka) {
-    case 1: kern = mxs::varlen_rows_kernel<KIND, 1>; break;
-    case 2: kern = mxs::varlen_rows_kernel<KIND, 2>; break;
-    case 3: kern = mxs::varlen_rows_kernel<KIND, 3>; break;
-    case 4: kern = mxs::varlen_rows_kernel<KIND, 4>; break;
+    case 1: kern = fuse ? mxs::varlen_rows_kernel<KIND, 1, true> : mxs::varlen_rows_kernel<KIND, 1, false>; break;
+    case 2: kern = fuse ? mxs::varlen_rows_kernel<KIND, 2, true> : mxs::varlen_rows_kernel<KIND, 2, false>; break;
+    case 3: kern = fuse ? mxs::varlen_rows_kernel<KIND, 3, true> : mxs::varlen_rows_kernel<KIND, 3, false>; break;
+    case 4: kern = fuse ? mxs::varlen_rows_kernel<KIND, 4, true> : mxs::varlen_rows_kernel<KIND, 4, false>; break;
     default: return MXS_UNSUPPORTED;
   }
   const size_t smem = mxs::varlen_rows_smem_bytes(ka, stages);

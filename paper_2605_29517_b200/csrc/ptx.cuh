@@ -294,6 +294,11 @@ MXS_DEV uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
+MXS_DEV float ld_cluster_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
 MXS_DEV void st_cluster_f32(uint32_t cluster_addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
 }
@@ -314,6 +319,29 @@ MXS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   }
+}
+// Same with the suspend-time hint (the waiting warp yields its issue slots while it waits): for
+// warps that mostly wait, like the fused-score warps, so they do not slow the epilogue warps of
+// their SM sub-partition.
+MXS_DEV void mbar_wait_cluster_idle(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+template <int CL>
+MXS_DEV void mbar_wait_cl_idle(uint64_t* bar, uint32_t parity) {
+  if constexpr (CL == 1)
+    mbar_wait_idle(bar, parity);
+  else
+    mbar_wait_cluster_idle(bar, parity);
 }
 // Cluster-size-generic forms: CL == 1 stays on the CTA-local instructions.
 template <int CL>

@@ -43,19 +43,25 @@ struct CertSum {
   }
 };
 
-// Whole warp: S4 score of v[0..n) (global or shared memory).  The result is valid in every lane.
-MXS_DEV double warp_score_sum(const float* v, int n) {
+// Whole warp: S4 score of the n values load(0..n-1).  The result is valid in every lane.
+template <typename Load>
+MXS_DEV double warp_score_sum_fn(int n, Load load) {
   const int lane = (int)(threadIdx.x & 31u);
   CertSum c;
-  for (int i = lane; i < n; i += 32) c.add(v[i]);
+  for (int i = lane; i < n; i += 32) c.add(load(i));
   c.warp_reduce();
   if (c.exact(n)) return c.s;
   double t = 0.0;  // sequential fallback (rare): the reference order itself
   if (lane == 0) {
-    t = (double)v[0];
-    for (int i = 1; i < n; ++i) t = __dadd_rn(t, (double)v[i]);
+    t = (double)load(0);
+    for (int i = 1; i < n; ++i) t = __dadd_rn(t, (double)load(i));
   }
   return __shfl_sync(0xffffffffu, t, 0);
+}
+
+// Whole warp: S4 score of v[0..n) (global or shared memory).
+MXS_DEV double warp_score_sum(const float* v, int n) {
+  return warp_score_sum_fn(n, [v](int i) { return v[i]; });
 }
 
 }  // namespace mxs

@@ -43,6 +43,7 @@ struct VarlenRowsParams {
 
 constexpr int kVrTile = 128;       // tokens per tile (MMA N)
 constexpr int kVrThreads = 32 * 15;  // warp 0 TMA, 1 MMA + TMEM, 2..9 scan, 10 boundaries, 11..14 merge
+constexpr int kVrSumWarp = 12;       // fused kernels (n_cols <= 32, merge warps 12..14 idle): S4 sum warp
 constexpr int kVrSlotCols = 128;
 constexpr int kVrSlots = 4;
 constexpr int kVrInfoSlots = 16;
@@ -102,39 +103,78 @@ MXS_DEV long long vr_row_base(const VarlenRowsParams& p, int row) {
   const int q = r / p.l_q, i = r - q * p.l_q;
   return (long long)q * p.n_docs * p.l_q + i;
 }
-// Whole warp (warp-uniform doc): S4 score of every query whose l_q rows are lanes
-// [k * l_q, (k + 1) * l_q) of the warp.  Lanes without a row (rbase < 0) contribute nothing.
-__device__ __noinline__ void vr_emit_score(const VarlenRowsParams& p, long long rbase, long long doc, float m) {
-  if (doc < 0) return;
-  const int lane = (int)(threadIdx.x & 31u);
-  const int seg = p.l_q;  // power of two <= 32
-  const bool valid = rbase >= 0;
-  CertSum c;
-  if (valid) c.add(m);
-  int fin = c.finite ? 1 : 0;
-  for (int o = seg >> 1; o; o >>= 1) {  // segmented butterfly: xor offsets < seg stay in the segment
-    c.s += __shfl_xor_sync(0xffffffffu, c.s, o);
-    c.emin = min(c.emin, __shfl_xor_sync(0xffffffffu, c.emin, o));
-    c.emax = max(c.emax, __shfl_xor_sync(0xffffffffu, c.emax, o));
-    fin = min(fin, __shfl_xor_sync(0xffffffffu, fin, o));
-  }
-  c.finite = fin != 0;
-  const bool lead = valid && (lane & (seg - 1)) == 0;
-  const bool ex = c.exact(seg);
-  double sc = c.s;
-  if (__any_sync(0xffffffffu, lead && !ex)) {  // sequential chain (rare): the reference order
-    double t = 0.0;
-    for (int i = 0; i < seg; ++i) {
-      const float v = __shfl_sync(0xffffffffu, m, (lane & ~(seg - 1)) + i);
-      t = (i == 0) ? (double)v : __dadd_rn(t, (double)v);
-    }
-    if (!ex) sc = t;
-  }
-  if (lead) p.scores[rbase / ((long long)p.n_docs * p.l_q) * p.n_docs + doc] = sc;
+// Fused S4 ring (fused kernels only, n_cols <= 32: one emission = one document for ALL query
+// rows).  The emitting scan / merge warp only stores its 32 row maxima into a slot of this ring
+// and arrives on the slot's mbarrier (a few instructions); the sum warp folds the slots in
+// allocation order, waiting on the mbarriers with the suspend hint so that it takes no issue slots
+// from the scan / merge warps.  Putting the warp reduction itself at the emission sites cost the
+// HBM-bound scan ~50 %.
+constexpr int kVrRing = 32;
+struct VrRing {
+  float m[kVrRing][32];
+  long long doc[kVrRing];
+  uint64_t full[kVrRing];   // 32 arrivals: the emitting warp's lanes wrote slot k % kVrRing
+  uint64_t empty[kVrRing];  // 1 arrival: the sum warp consumed it
+  uint32_t tail;            // emissions allocated so far
+};
+__shared__ VrRing vr_ring;
+
+MXS_DEV void vr_push(long long doc, float m) {
+  if (doc < 0) return;  // warp-uniform
+  const uint32_t lane = lane_id();
+  uint32_t k = 0;
+  if (lane == 0) k = atomicAdd(&vr_ring.tail, 1u);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  const uint32_t s = k % kVrRing, gen = k / kVrRing;
+  mbar_wait(&vr_ring.empty[s], (gen & 1u) ^ 1u);  // the slot's previous generation was consumed
+  vr_ring.m[s][lane] = m;
+  if (lane == 0) vr_ring.doc[s] = doc;
+  mbar_arrive(&vr_ring.full[s]);  // release: orders this lane's stores
 }
 
+// Sum warp: the CTA's documents in emission order; per slot, the S4 score of every query whose
+// l_q rows are lanes [k * l_q, (k + 1) * l_q) (l_q divides 32, rows = lanes < n_cols).
+MXS_DEV void vr_sum_warp(const VarlenRowsParams& p, long long n_emit) {
+  const int lane = (int)lane_id();
+  const int seg = p.l_q;
+  const bool valid = lane < p.n_cols;
+  const bool lead = valid && (lane & (seg - 1)) == 0;
+  for (long long n = 0; n < n_emit; ++n) {
+    const uint32_t s = (uint32_t)(n % kVrRing), gen = (uint32_t)(n / kVrRing);
+    mbar_wait_idle(&vr_ring.full[s], gen & 1u);
+    const float m = vr_ring.m[s][lane];
+    const long long doc = vr_ring.doc[s];
+    CertSum c;
+    if (valid) c.add(m);
+    int fin = c.finite ? 1 : 0;
+    for (int o = seg >> 1; o; o >>= 1) {  // segmented butterfly: xor offsets < seg stay in the segment
+      c.s += __shfl_xor_sync(0xffffffffu, c.s, o);
+      c.emin = min(c.emin, __shfl_xor_sync(0xffffffffu, c.emin, o));
+      c.emax = max(c.emax, __shfl_xor_sync(0xffffffffu, c.emax, o));
+      fin = min(fin, __shfl_xor_sync(0xffffffffu, fin, o));
+    }
+    c.finite = fin != 0;
+    const bool ex = c.exact(seg);
+    double sc = c.s;
+    if (__any_sync(0xffffffffu, lead && !ex)) {  // sequential chain (rare): the reference order
+      double t = 0.0;
+      for (int i = 0; i < seg; ++i) {
+        const float v = __shfl_sync(0xffffffffu, m, (lane & ~(seg - 1)) + i);
+        t = (i == 0) ? (double)v : __dadd_rn(t, (double)v);
+      }
+      if (!ex) sc = t;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&vr_ring.empty[s]);  // every lane has consumed its value (c / sc above)
+    if (lead) p.scores[(long long)((p.row0 + lane) / seg) * p.n_docs + doc] = sc;
+  }
+}
+
+// FUSED is a compile-time choice: the non-fused kernels carry no trace of the warp reduction (its
+// mere presence at the emission sites cost the HBM-bound scan ~40 % through code generation).
+template <bool FUSED>
 MXS_DEV void vr_emit(const VarlenRowsParams& p, long long rbase, long long doc, float m, long long arg_local) {
-  if (p.scores) vr_emit_score(p, rbase, doc, m);
+  if constexpr (FUSED) vr_push(doc, m);
   if (rbase < 0 || doc < 0) return;
   const long long o = rbase + doc * p.l_q;
   if (p.rowmax) p.rowmax[o] = m;
@@ -174,7 +214,7 @@ MXS_DEV bool vr_bit(const uint32_t (&w)[4], int x) { return (w[x >> 5] >> (x & 3
 // Documents that start and end inside the range are written out directly; the range's head
 // piece (before its first document start) and tail piece (from its last start) go to shared
 // memory for the merge warp.
-template <TcKind KIND, int KA, int C>
+template <TcKind KIND, int KA, int C, bool FUSED>
 MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh, uint32_t tmem_base, int set,
                      int quad, uint32_t lane, int n_tiles, long long tok_begin, long long tok_end) {
   constexpr int L = kVrTile / C;        // tokens per range
@@ -234,27 +274,75 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
               m = fmaxf(m, v);
             }
           } else {
+            const int nv = min(32, x1 - xb);
+            uint32_t starts = word & (nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u));
+            if (__popc(starts) <= 1) {
+              // Common case (documents of >= 32 tokens): one start in the chunk.  Single in-order
+              // pass; the document it closes is emitted after the unrolled loop, so the emission
+              // code exists once.
+              bool pend = false;
+              float pm = -INFINITY;
+              int pa = 0;
+              long long pdoc = 0, pds = 0;
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              if (xb + q < x1) {
-                if ((word >> q) & 1u) {  // token xb + q starts document doc + 1 (warp-uniform)
-                  if (in_head) {
-                    hm = m;
-                    ha = a;
-                    in_head = false;
-                  } else {
-                    vr_emit(p, rbase, doc, m, p0 + a - dstart);  // complete inside this range
+              for (int q = 0; q < 32; ++q) {
+                if (q < nv) {
+                  if ((starts >> q) & 1u) {  // token xb + q starts document doc + 1 (warp-uniform)
+                    if (in_head) {
+                      hm = m;
+                      ha = a;
+                      in_head = false;
+                    } else {  // complete inside this range
+                      pend = true;
+                      pm = m;
+                      pa = a;
+                      pdoc = doc;
+                      pds = dstart;
+                    }
+                    ++doc;
+                    dstart = p0 + xb + q;
+                    m = -INFINITY;
+                    a = 0;
                   }
-                  ++doc;
-                  dstart = p0 + xb + q;
-                  m = -INFINITY;
-                  a = 0;
+                  const float v = __uint_as_float(r[q]);
+                  if (v > m) {
+                    m = v;
+                    a = xb + q;
+                  }
                 }
-                const float v = __uint_as_float(r[q]);
-                if (v > m) {
-                  m = v;
-                  a = xb + q;
+              }
+              if (pend) vr_emit<FUSED>(p, rbase, pdoc, pm, p0 + pa - pds);
+            } else {
+              // Several starts (documents shorter than a range): one rolled iteration per piece,
+              // tokens [s, e) folded in order by a predicated unrolled pass (r[] stays in
+              // registers), then the document ending at start e is closed.
+              int s = 0;
+#pragma unroll 1
+              for (;;) {
+                const int e = starts ? __ffs((int)starts) - 1 : nv;
+                const uint32_t seg = (e >= 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((1u << s) - 1u);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                  const float v = __uint_as_float(r[q]);
+                  if (((seg >> q) & 1u) && v > m) {
+                    m = v;
+                    a = xb + q;
+                  }
                 }
+                if (!starts) break;
+                if (in_head) {
+                  hm = m;
+                  ha = a;
+                  in_head = false;
+                } else {
+                  vr_emit<FUSED>(p, rbase, doc, m, p0 + a - dstart);
+                }
+                ++doc;
+                dstart = p0 + xb + e;
+                m = -INFINITY;
+                a = 0;
+                starts &= starts - 1u;
+                s = e;
               }
             }
           }
@@ -293,7 +381,7 @@ struct VrTileFold {
   int pa = 0, plast = 0;    // its max position and its start (tile offsets)
   long long pd = 0;         // its document
 };
-template <int C, bool FULL>
+template <int C, bool FULL, bool FUSED>
 MXS_DEV void vr_fold_ranges(VrTileFold& f, const float* hm, const int16_t* ha, const float* tm, const int16_t* ta,
                             const uint32_t (&w)[4], long long d_first, int ntok, int row, const VarlenRowsParams& p,
                             long long rbase) {
@@ -326,7 +414,7 @@ MXS_DEV void vr_fold_ranges(VrTileFold& f, const float* hm, const int16_t* ha, c
       }
     }
     if (st || nb) {  // the current piece ends at the range's first start
-      if (f.seen) vr_emit(p, rbase, f.pd, f.pm, f.pa - f.plast);
+      if (f.seen) vr_emit<FUSED>(p, rbase, f.pd, f.pm, f.pa - f.plast);
       f.seen = true;
       f.plast = vr_last_bit(w, r0, r1);
       f.pd = d_first + vr_popc_range(w, 1, r1);
@@ -339,7 +427,7 @@ MXS_DEV void vr_fold_ranges(VrTileFold& f, const float* hm, const int16_t* ha, c
 // Merge warp for query rows [32 j, 32 j + 32): walks ALL tiles in order, folds the ranges of each
 // tile (token order, strict >) and carries the document still open at the tile's end in
 // registers -- the only serial work of the kernel, ~100 instructions per tile.
-template <int C>
+template <int C, bool FUSED>
 MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh, int j, uint32_t lane, int n_tiles,
                       long long tok_begin, long long tok_end) {
   constexpr int L = kVrTile / C;
@@ -363,10 +451,10 @@ MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh
     mbar_wait(&hdr->pfull[set][pb], (((uint32_t)t >> 1) / kVrPieceBufs) & 1u);
     VrTileFold f;
     if (ntok == kVrTile)
-      vr_fold_ranges<C, true>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
+      vr_fold_ranges<C, true, FUSED>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
                               kVrTile, row, p, rbase);
     else
-      vr_fold_ranges<C, false>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
+      vr_fold_ranges<C, false, FUSED>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
                                ntok, row, p, rbase);
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr->pempty[set][pb]);
@@ -375,17 +463,17 @@ MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh
       ca = p0 + f.tha;
     }
     if (f.seen) {  // the carried document ended at the tile's first start
-      vr_emit(p, rbase, cd, cm, ca - cs);
+      vr_emit<FUSED>(p, rbase, cd, cm, ca - cs);
       cm = f.pm;
       ca = p0 + f.pa;
       cd = f.pd;
       cs = p0 + f.plast;
     }
   }
-  if (n_tiles > 0) vr_emit(p, rbase, cd, cm, ca - cs);  // the CTA's last document ends at tok_end
+  if (n_tiles > 0) vr_emit<FUSED>(p, rbase, cd, cm, ca - cs);  // the CTA's last document ends at tok_end
 }
 
-template <TcKind KIND, int KA>
+template <TcKind KIND, int KA, bool FUSED>
 __global__ void __launch_bounds__(kVrThreads, 1)
     varlen_rows_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmQ,
                        const VarlenRowsParams p) {
@@ -433,6 +521,14 @@ __global__ void __launch_bounds__(kVrThreads, 1)
         mbar_init(&hdr->pempty[s][b], (uint32_t)n_merge);
       }
     fence_mbar_init();
+  }
+  if constexpr (FUSED) {
+    if (warp == kVrSumWarp) {
+      mbar_init(&vr_ring.full[lane], 32);
+      mbar_init(&vr_ring.empty[lane], 1);
+      if (lane == 0) vr_ring.tail = 0u;
+      fence_mbar_init();
+    }
   }
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
   tc_fence_before();
@@ -555,25 +651,36 @@ __global__ void __launch_bounds__(kVrThreads, 1)
       }
       __syncwarp();
     }
+  } else if (FUSED && warp == kVrSumWarp) {
+    // ------------------------------------------------------------------ fused S4 sum
+    vr_sum_warp(p, hdr->doc_end - hdr->doc_begin);
   } else if (warp >= 11) {
     // ------------------------------------------------------------------ merge
     const int j = (int)warp - 11;
-    if (C == 4)
-      vr_merge<4>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
-    else if (C == 2)
-      vr_merge<2>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
-    else
-      vr_merge<1>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+    if constexpr (FUSED) {  // fused kernels: n_cols <= 32 (C = 4) only
+      vr_merge<4, true>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+    } else {
+      if (C == 4)
+        vr_merge<4, false>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+      else if (C == 2)
+        vr_merge<2, false>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+      else
+        vr_merge<1, false>(p, hdr, sh, j, lane, n_tiles, tok_begin, tok_end);
+    }
   } else {
     // ------------------------------------------------------------------ scan
     const int set = ((int)warp - 2) >> 2;  // tiles t with t % 2 == set, TMEM slots set and set + 2
     const int quad = (int)(warp & 3);      // TMEM lane quadrant (hardware rule: warp id % 4)
-    if (C == 4)
-      vr_scan<KIND, KA, 4>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
-    else if (C == 2)
-      vr_scan<KIND, KA, 2>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
-    else
-      vr_scan<KIND, KA, 1>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+    if constexpr (FUSED) {
+      vr_scan<KIND, KA, 4, true>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+    } else {
+      if (C == 4)
+        vr_scan<KIND, KA, 4, false>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+      else if (C == 2)
+        vr_scan<KIND, KA, 2, false>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+      else
+        vr_scan<KIND, KA, 1, false>(p, hdr, sh, tmem_base, set, quad, lane, n_tiles, tok_begin, tok_end);
+    }
   }
   tc_fence_before();
   __syncthreads();

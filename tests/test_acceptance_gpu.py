@@ -303,7 +303,7 @@ def test_c5_1m_docs_sampled_vs_oracle_and_shard_invariance():
         assert torch.equal(a_r, am[:, a:b]), f"shard {r} argmax differs"
     # >= 1000 sampled documents: 24 around every shard boundary + random ones, vs the oracle
     rng = np.random.default_rng(9)
-    pick = set(rng.choice(n, 800, replace=False).tolist())
+    pick = set(rng.choice(n, 900, replace=False).tolist())
     for a, _ in bounds:
         pick |= set(range(max(0, a - 12), min(n, a + 12)))
     pick |= {0, n - 1}
