@@ -522,9 +522,11 @@ def test_scores_without_argmax_are_identical():
     lens = rng.integers(1, 400, 37).astype(np.int32)
     D, vl = orc.padded(orc.make_corpus(37, lens, 128, seed=4), 400)
     Dt, vlt = cuda(D, torch.bfloat16), cuda(vl)
-    s1, a1, r1 = mx.score_dense(Q, Dt, vlt)
-    s2, a2, r2 = mx.score_dense(Q, Dt, vlt, want_argmax=False)
+    s1, a1, r1 = mx.score_dense(Q, Dt, vlt, want_rowmax=True)
+    s2, a2, r2 = mx.score_dense(Q, Dt, vlt, want_argmax=False, want_rowmax=True)
     assert a2 is None and torch.equal(s1, s2) and torch.equal(r1, r2)
+    s3, a3, r3 = mx.score_dense(Q, Dt, vlt, want_argmax=False)  # fused S4, no row maxima materialised
+    assert r3 is None and torch.equal(s3, s1)
 
 
 # ------------------------------------------------------------------ top-K (K9)
