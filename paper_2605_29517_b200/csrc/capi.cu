@@ -9,6 +9,7 @@
 
 #include "host.h"
 #include "mxs1_io.h"
+#include <exception>
 
 using namespace mxs_host;
 
@@ -246,7 +247,9 @@ static int mxs1_truncated(int64_t expected, int64_t actual) {
               (long long)actual);
 }
 
-int mxs_mxs1_open(const char* path, void** handle) {
+static int mxs1_read_block_impl(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes);
+
+static int mxs1_open_impl(const char* path, void** handle) {
   if (!path || !handle) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_open: null pointer");
   *handle = nullptr;
   const int fd = ::open(path, O_RDONLY | O_CLOEXEC);
@@ -286,15 +289,48 @@ int mxs_mxs1_open(const char* path, void** handle) {
     out = (int64_t)v;  // little-endian host (x86-64 / aarch64)
     return true;
   };
+  // Header sizes come from an untrusted file: every count and byte product is checked against
+  // the file size before anything is allocated (a hostile n_docs must raise TruncatedPayload the
+  // way the reference's short read does, not abort the process with bad_alloc).
   if (lc == mxs_io::kDense || lc == mxs_io::kQuantized) {
     if (!u64(f->n_docs) || !u64(f->length) || !u64(f->dim)) return bail(MXS_TRUNCATED_PAYLOAD);
+    const int64_t avail = f->file_size > off ? f->file_size - off : 0;
+    int64_t need = 0;
+    if (!mxs_io::payload_bytes(f->n_docs, f->length, f->dim, mxs_io::elem_size(ec), lc == mxs_io::kQuantized, &need))
+      return bail(fail(MXS_TRUNCATED_PAYLOAD, "payload truncated: expected %llu bytes, file holds %lld",
+                       (unsigned long long)UINT64_MAX, (long long)avail));
+    (void)need;  // a short payload is reported lazily by the block reads (streaming reads a prefix)
   } else {
     if (!u64(f->n_docs) || !u64(f->dim)) return bail(MXS_TRUNCATED_PAYLOAD);
-    f->cu.resize((size_t)f->n_docs + 1);
+    const int64_t avail = f->file_size > off ? f->file_size - off : 0;
+    // 8 * (n_docs + 1) offsets must fit in what is left of the file (n_docs < 0 = top bit set)
+    if (f->n_docs < 0 || f->n_docs >= avail / 8) {
+      const unsigned long long want = (f->n_docs < 0 || f->n_docs > (INT64_MAX / 8 - 1))
+                                          ? (unsigned long long)UINT64_MAX
+                                          : (unsigned long long)(8 * (f->n_docs + 1));
+      return bail(fail(MXS_TRUNCATED_PAYLOAD, "payload truncated: expected %llu bytes, file holds %lld", want,
+                       (long long)avail));
+    }
     const int64_t need = 8 * (f->n_docs + 1);
+    try {
+      f->cu.resize((size_t)f->n_docs + 1);
+    } catch (...) {
+      return bail(fail(MXS_IO_ERROR, "cannot allocate the offset table of %lld documents", (long long)f->n_docs));
+    }
     const int64_t got = mxs_io::pread_all(fd, f->cu.data(), need, off);
     if (got != need) return bail(mxs1_truncated(need, got < 0 ? 0 : got));
     off += need;
+    // PackedCorpus invariants (maxsim/varlen.py:36-41): cu[0] = 0, strictly increasing, and the
+    // token payload cu[B] * dim fits in the file
+    if (f->cu[0] != 0)
+      return bail(fail(MXS_SHAPE_MISMATCH, "cu_seqlens must be 1-D with cu[0] = 0 and one entry per document plus one"));
+    for (int64_t b = 0; b < f->n_docs; ++b)
+      if (f->cu[(size_t)b + 1] <= f->cu[(size_t)b]) return bail(fail(MXS_EMPTY_DOCUMENT, "document %lld has no valid tokens", (long long)b));
+    const int64_t avail2 = f->file_size > off ? f->file_size - off : 0;
+    int64_t need_t = 0;
+    if (!mxs_io::payload_bytes(f->cu.back(), 1, f->dim, mxs_io::elem_size(ec), false, &need_t))
+      return bail(fail(MXS_TRUNCATED_PAYLOAD, "payload truncated: expected %llu bytes, file holds %lld",
+                       (unsigned long long)UINT64_MAX, (long long)avail2));
   }
   if (lc == mxs_io::kQuantized && ec != mxs_io::kI8)
     return bail(fail(MXS_BAD_MAGIC, "quantized layout requires the i8 element tag"));
@@ -303,6 +339,28 @@ int mxs_mxs1_open(const char* path, void** handle) {
   f->payload_offset = off;
   *handle = f;
   return MXS_OK;
+}
+
+// The host-side reader allocates (the header object, the offset table) and spawns pread threads:
+// no C++ exception may cross the extern "C" / ctypes boundary, so both entry points map one to a status.
+int mxs_mxs1_open(const char* path, void** handle) {
+  try {
+    return mxs1_open_impl(path, handle);
+  } catch (const std::exception& e) {
+    return fail(MXS_IO_ERROR, "cannot read %s: %s", path ? path : "(null)", e.what());
+  } catch (...) {
+    return fail(MXS_IO_ERROR, "cannot read %s: unknown error", path ? path : "(null)");
+  }
+}
+
+int mxs_mxs1_read_block(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes) {
+  try {
+    return mxs1_read_block_impl(handle, first, count, dst, dst_bytes);
+  } catch (const std::exception& e) {
+    return fail(MXS_IO_ERROR, "mxs_mxs1_read_block: %s", e.what());
+  } catch (...) {
+    return fail(MXS_IO_ERROR, "mxs_mxs1_read_block: unknown error");
+  }
 }
 
 int mxs_mxs1_info(void* handle, int32_t* elem, int32_t* layout, int64_t* n_docs, int64_t* length, int64_t* dim) {
@@ -346,7 +404,7 @@ int64_t mxs_mxs1_block_bytes(void* handle, int64_t first, int64_t count) {
   return bytes;
 }
 
-int mxs_mxs1_read_block(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes) {
+static int mxs1_read_block_impl(void* handle, int64_t first, int64_t count, void* dst, size_t dst_bytes) {
   auto* f = static_cast<mxs_io::Mxs1File*>(handle);
   if (!f || !dst) return fail(MXS_INVALID_ARGUMENT, "mxs_mxs1_read_block: null pointer");
   int64_t off = 0, bytes = 0;

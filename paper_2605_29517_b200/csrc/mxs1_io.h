@@ -38,6 +38,22 @@ struct Mxs1File {
 
 inline int elem_size(int elem) { return elem == kF32 ? 4 : (elem == kF16 ? 2 : 1); }
 
+// Payload bytes of n_docs x length x dim elements (+ n_docs x length f32 scales when quantized);
+// false when a header field is negative (top bit set) or the product overflows int64.
+inline bool payload_bytes(int64_t n_docs, int64_t length, int64_t dim, int64_t es, bool scales, int64_t* out) {
+  if (n_docs < 0 || length < 0 || dim < 0) return false;
+  int64_t rows = 0, elems = 0, bytes = 0, sbytes = 0;
+  if (__builtin_mul_overflow(n_docs, length, &rows)) return false;
+  if (__builtin_mul_overflow(rows, dim, &elems)) return false;
+  if (__builtin_mul_overflow(elems, es, &bytes)) return false;
+  if (scales) {
+    if (__builtin_mul_overflow(rows, (int64_t)4, &sbytes)) return false;
+    if (__builtin_add_overflow(bytes, sbytes, &bytes)) return false;
+  }
+  *out = bytes;
+  return true;
+}
+
 // Reads exactly n bytes at off (any number of pread calls); returns bytes read.
 inline int64_t pread_all(int fd, void* dst, int64_t n, int64_t off) {
   int64_t done = 0;

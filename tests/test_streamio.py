@@ -107,6 +107,35 @@ def test_reader_errors(tmp_path):
     r.close()
 
 
+def test_reader_hostile_headers(tmp_path):
+    """Untrusted header counts raise the reference's error classes instead of aborting the
+    process: the offset table of a packed file is sized against the file before it is allocated,
+    products that overflow int64 are refused, and the PackedCorpus invariants
+    (maxsim/varlen.py:36-41) hold for what the reader hands out."""
+    head = b"MXS1" + struct.pack("<H", 1)
+
+    def write(name, body):
+        p = tmp_path / name
+        p.write_bytes(body)
+        return str(p)
+
+    for n_docs in (1 << 40, (1 << 63) + 5, (1 << 64) - 1):  # huge, and top bit set (negative as int64)
+        path = write(f"n{n_docs}", head + bytes([0, 1]) + struct.pack("<QQ", n_docs, 16) + b"\0" * 64)
+        with pytest.raises(mx.TruncatedPayload) as ei:
+            streamio.CorpusReader(path)
+        assert ei.value.actual == 64 and ei.value.expected > 64
+    # dense: n_docs * length * dim * 4 overflows int64
+    with pytest.raises(mx.TruncatedPayload):
+        streamio.CorpusReader(write("ovf", head + bytes([0, 0]) + struct.pack("<QQQ", 1 << 40, 1 << 20, 1 << 10)))
+    # packed offset table: cu[0] != 0, an empty document, a decreasing offset
+    for cu, err in (([1, 3, 5], mx.ShapeMismatch), ([0, 3, 3], mx.EmptyDocument), ([0, 3, 2], mx.EmptyDocument)):
+        body = head + bytes([0, 1]) + struct.pack("<QQ", len(cu) - 1, 4) + struct.pack(f"<{len(cu)}Q", *cu)
+        with pytest.raises(err) as ei:
+            streamio.CorpusReader(write("cu", body + b"\0" * 80))
+        if err is mx.EmptyDocument:
+            assert ei.value.index == 1
+
+
 # ------------------------------------------------------------------ writer (CPU)
 def test_writer_reproduces_reference_files(tmp_path):
     e = expected()
