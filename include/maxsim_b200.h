@@ -138,7 +138,11 @@ int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, 
  *   dest_len  [n_docs] int64 destination rows owned by each document (padded_len or doc_len)
  *   row_ptr   [n_dest + 1] int32, col_idx [n_q * n_docs * l_q] int32 (ascending source id per
  *             bucket, i.e. the reference's stable argsort)
- *   ws        >= mxs_csr_workspace_bytes(n_q, n_dest) bytes of device scratch
+ *   ws        unused (mxs_csr_workspace_bytes returns 0; kept for ABI stability, may be NULL):
+ *             documents of up to ~14K rows build in one cluster-per-document kernel with
+ *             shared-memory histograms, longer ones (Chamfer clouds) through a stable radix sort
+ *             with stream-ordered scratch (cudaMallocAsync)
+ *   dest ranges [dest_off[b], dest_off[b] + dest_len[b]) must tile [0, n_dest)
  */
 size_t mxs_csr_workspace_bytes(int64_t n_q, int64_t n_dest);
 int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, int64_t l_q, const int64_t* dest_off,

@@ -5,7 +5,7 @@
 //   distance   : d = fl(fl(fl(<p,s>) * -2) + |p|^2) + |s|^2 with <p,s> the S1 sequential fold
 //                (maxsim/kernels.py:29-38, 50-66)
 //   fold       : strict <, columns ascending -> lowest index on ties (maxsim/kernels.py:69-93)
-// Point clouds are 3-D (dim generic, <= kChDimMax): K = 3 gives a tensor core nothing to do, so
+// Point clouds are 3-D (any dim; <= kChDimMax keeps the point in registers): K = 3 gives a tensor core nothing to do, so
 // this is an FP32-ALU kernel -- one thread per point of the first set, the second set streamed
 // through shared memory in tiles, every product / add an explicit _rn intrinsic (no FMA
 // contraction) so the bits match numpy's.
@@ -69,6 +69,49 @@ __global__ void __launch_bounds__(kChThreads) chamfer_nn_kernel(const float* __r
           if (k < D) dot = __fadd_rn(dot, __fmul_rn(a[k], b[k]));
         const float d = __fadd_rn(__fadd_rn(__fmul_rn(dot, -2.0f), ai), sBn[j]);
         if (d < bd) {  // strict: the lowest index wins ties
+          bd = d;
+          bj = (int)(t0 + j);
+        }
+      }
+    }
+  }
+  if (i < n) {
+    best[i] = bd;
+    idx[i] = bj;
+  }
+}
+
+// Any dimension (> kChDimMax): the point of the first set stays in global memory (L1-resident,
+// one row per thread), the second set streams through shared memory in tiles of 8192 floats.
+// Same S1 fold, same strict-< scan, so the bits match the register kernel's and the reference's.
+__global__ void __launch_bounds__(kChThreads) chamfer_nn_any_kernel(const float* __restrict__ A,
+                                                                    const float* __restrict__ an, long long n,
+                                                                    const float* __restrict__ B,
+                                                                    const float* __restrict__ bn, long long m,
+                                                                    int dim, float* __restrict__ best,
+                                                                    int32_t* __restrict__ idx) {
+  constexpr int kFloats = 8192;
+  __shared__ float sB[kFloats];
+  __shared__ float sBn[kFloats / (kChDimMax + 1) + 1];  // dim > kChDimMax -> tile <= 481
+  const int tile = max(1, kFloats / dim);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const float* a = A + (i < n ? i : 0) * dim;
+  const float ai = i < n ? an[i] : 0.f;
+  float bd = INFINITY;
+  int bj = 0;
+  for (long long t0 = 0; t0 < m; t0 += tile) {
+    const int cnt = (int)min((long long)tile, m - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * dim; e += blockDim.x) sB[e] = B[t0 * dim + e];
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) sBn[e] = bn[t0 + e];
+    __syncthreads();
+    if (i < n) {
+      for (int j = 0; j < cnt; ++j) {
+        const float* b = sB + j * dim;
+        float dot = __fmul_rn(a[0], b[0]);
+        for (int k = 1; k < dim; ++k) dot = __fadd_rn(dot, __fmul_rn(a[k], b[k]));
+        const float d = __fadd_rn(__fadd_rn(__fmul_rn(dot, -2.0f), ai), sBn[j]);
+        if (d < bd) {
           bd = d;
           bj = (int)(t0 + j);
         }

@@ -3,265 +3,279 @@
 //
 // Source s = (q * B + b) * L_q + i picks destination row dest_off[b] + argmax[s].  Every source
 // of document b lands in b's rows, so b's bucket block starts at row_ptr = b * N_q * L_q and the
-// problem splits per document.  Stability (ascending s inside each bucket) is ascending (q, i)
-// within the document, obtained in three passes without global atomics:
-//   1. csr_count_kernel   block (q, b): smem histogram of argmax[q, b, :] -> cnt[q][dest row]
-//   2. csr_scan_kernel    block b: totals over q, exclusive scan over b's rows -> row_ptr;
-//                         cnt[q][r] becomes the first slot of segment (q, b) inside bucket r
-//   3. csr_place_kernel   block (q, b): stable in-segment ranks (warp match + warp-ordered
-//                         cursor updates) -> col_idx[slot] = s
+// problem splits per document; inside a document, ascending s is ascending flat j = q * L_q + i.
+//
+// csr_doc_kernel -- ONE launch, no global workspace: a thread-block cluster of CL CTAs owns one
+// document.  Its N_q * L_q sources (flat j) are cut into CL * W contiguous warp ranges, in order.
+//   1. count:  every warp builds a shared-memory histogram of its range's destinations
+//   2. prefix: per bucket, an exclusive prefix over the CTA's warps (in place) and the CTA total
+//   3. cluster barrier; every CTA reads the other CTAs' totals through DSMEM: bucket base
+//      (exclusive scan over the document's rows, one block scan) + the totals of lower ranks
+//      -> each warp's first slot in every bucket.  Rank 0 writes row_ptr.
+//   4. place:  every warp walks its range in source order, 32 keys per step; equal keys inside a
+//      step are grouped through a byte tag per bucket + 5 ballots (8 steps interleaved), ranked
+//      by lane, and the lowest lane of each group advances the bucket cursor.
+// The CSR is therefore the stable counting sort the reference computes, with no atomics on
+// global memory and one pass over argmax for the count plus one (L2-resident) for the placement.
+//
+// csr_sort_* -- the general path for destinations too long for shared-memory histograms
+// (Chamfer clouds, documents beyond ~3K rows): a stable LSD radix sort of (dest row, source)
+// pairs (cub::DeviceRadixSort, stable by construction) and row_ptr by binary search.
 // Indices are int32 (n_src and n_dest < 2^31 are checked on the host).
 #pragma once
 #include "ptx.cuh"
 
 namespace mxs {
 
+// n / d for 32-bit unsigned n and a run-time invariant d >= 1 (Granlund-Montgomery): a mulhi, a
+// subtract and two shifts instead of the ~20-instruction division subroutine per source.
+struct FastDiv {
+  uint32_t d, m, s1, s2;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while (l < 32 && (1ull << l) < d) ++l;
+  FastDiv f;
+  f.d = d;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  f.s1 = l < 1 ? l : 1;
+  f.s2 = l > 1 ? l - 1 : 0;
+  return f;
+}
+MXS_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  const uint32_t t = __umulhi(n, f.m);
+  return (t + ((n - t) >> f.s1)) >> f.s2;
+}
+
+// A lane's walk over the flat sources j = q * L_q + i of one document in steps of 32: the source
+// id (which is also the argmax offset) advances incrementally (no division per step; L_q < 32
+// wraps in a loop).
+struct SrcWalk {
+  int src;  // (q * B + b) * L_q + i
+  int i;
+  MXS_DEV void init(uint32_t j, const FastDiv& lq, int l_q, int n_docs, int b) {
+    const uint32_t q = fdiv(j, lq);
+    i = (int)(j - q * (uint32_t)l_q);
+    src = (int)((q * (uint32_t)n_docs + (uint32_t)b) * (uint32_t)l_q) + i;
+  }
+  MXS_DEV void step32(int l_q, int wrap) {  // wrap = (B - 1) * L_q
+    i += 32;
+    src += 32;
+    while (i >= l_q) {
+      i -= l_q;
+      src += wrap;
+    }
+  }
+};
+
 struct CsrParams {
-  const int32_t* argmax;    // [n_q, B, l_q]
+  const int32_t* argmax;      // [n_q, B, l_q]
   const long long* dest_off;  // [B] first destination row of each document
   const long long* dest_len;  // [B] destination rows owned by each document
   int n_q, n_docs, l_q;
   long long n_dest;
-  int32_t* cnt;             // workspace [n_q][n_dest]
-  int32_t* row_ptr;         // [n_dest + 1]
-  int32_t* col_idx;         // [n_q * B * l_q]
+  int hist_len;               // >= every dest_len, multiple of 4 (shared-memory row stride)
+  FastDiv lq_div;             // division by l_q
+  int32_t* row_ptr;           // [n_dest + 1]
+  int32_t* col_idx;           // [n_q * B * l_q]
 };
 
-__global__ void __launch_bounds__(256) csr_count_kernel(const CsrParams p) {
-  extern __shared__ int32_t hist[];
-  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
-  const long long off = p.dest_off[b];
-  const int len = (int)p.dest_len[b];
-  for (int t = threadIdx.x; t < len; t += blockDim.x) hist[t] = 0;
-  __syncthreads();
-  const int32_t* a = p.argmax + ((long long)q * p.n_docs + b) * p.l_q;
-  for (int i = threadIdx.x; i < p.l_q; i += blockDim.x) {
-    const int t = a[i];
-    if (t >= 0 && t < len) atomicAdd(&hist[t], 1);
-  }
-  __syncthreads();
-  int32_t* out = p.cnt + (long long)q * p.n_dest + off;
-  for (int t = threadIdx.x; t < len; t += blockDim.x) out[t] = hist[t];
+MXS_DEV uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
 }
-
-// One block per document: rows [off, off + len).  Padding rows between documents (padded
-// layout) belong to the document before them and simply have zero count.
-__global__ void __launch_bounds__(1024) csr_scan_kernel(const CsrParams p) {
-  __shared__ int32_t warp_tot[32];
-  __shared__ int32_t carry;
-  const int b = blockIdx.x;
-  const long long off = p.dest_off[b];
-  const int len = (int)p.dest_len[b];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = (int32_t)((long long)b * p.n_q * p.l_q);
-  __syncthreads();
-  for (int t0 = 0; t0 < len; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
-    int tot = 0;
-    if (t < len) {
-#pragma unroll 16
-      for (int q = 0; q < p.n_q; ++q) tot += p.cnt[(long long)q * p.n_dest + off + t];  // 16 loads in flight
-    }
-    // block exclusive scan of tot
-    int x = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int v = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      warp_tot[lane] = v;  // inclusive
-    }
-    __syncthreads();
-    const int excl = carry + (w ? warp_tot[w - 1] : 0) + x - tot;
-    if (t < len) {
-      p.row_ptr[off + t] = excl;
-      int run = excl;
-      int q0 = 0;
-      for (; q0 + 16 <= p.n_q; q0 += 16) {  // 16 independent loads, then the running prefix
-        int v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = p.cnt[(long long)(q0 + u) * p.n_dest + off + t];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          p.cnt[(long long)(q0 + u) * p.n_dest + off + t] = run;
-          run += v[u];
-        }
-      }
-      for (int q = q0; q < p.n_q; ++q) {
-        int32_t* c = p.cnt + (long long)q * p.n_dest + off + t;
-        const int v = *c;
-        *c = run;
-        run += v;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + tot;
-    __syncthreads();
-  }
-  if (b == p.n_docs - 1 && threadIdx.x == 0) p.row_ptr[p.n_dest] = (int32_t)((long long)p.n_docs * p.n_q * p.l_q);
+MXS_DEV int32_t ld_cluster_s32(uint32_t cluster_addr) {
+  int32_t v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
+  return v;
 }
+MXS_DEV void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+MXS_DEV void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
-// One block per (q, b) segment; warps take turns in source order so that the per-bucket
-// cursor advances exactly as a sequential stable scatter would.
-__global__ void __launch_bounds__(256) csr_place_kernel(const CsrParams p) {
-  extern __shared__ int32_t cursor[];
-  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
-  const long long off = p.dest_off[b];
-  const int len = (int)p.dest_len[b];
-  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;
-  for (int t = threadIdx.x; t < len; t += blockDim.x) cursor[t] = base[t];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const long long src0 = ((long long)q * p.n_docs + b) * p.l_q;
-  const int32_t* a = p.argmax + src0;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int i0 = 0; i0 < p.l_q; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool valid = i < p.l_q;
-    const int key = valid ? a[i] : -1 - lane;  // distinct dummy keys never match real ones
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int rank = __popc(peers & lt_mask);
-    for (int ww = 0; ww < nw; ++ww) {
-      if (w == ww && valid) {
-        p.col_idx[cursor[key] + rank] = (int32_t)(src0 + i);
-      }
-      __syncwarp();
-      if (w == ww && valid && rank == 0) cursor[key] += __popc(peers);
-      __syncthreads();
-    }
-  }
-}
+constexpr int kCsrMaxWarps = 16;
 
-// Placement v2: one block per (q, b) segment, 8 warps on contiguous source chunks.  Per-warp
-// bucket histograms in shared memory turn the cross-warp order into prefix offsets, so every
-// warp places its chunk independently (in-warp order from __match_any_sync ranks) -- two block
-// barriers per segment instead of one per warp turn.
-constexpr int kCsrWarps = 8;
-__global__ void __launch_bounds__(32 * kCsrWarps) csr_place_v2_kernel(const CsrParams p) {
-  extern __shared__ int32_t hw[];  // [kCsrWarps][len]
-  const int q = blockIdx.x / p.n_docs, b = blockIdx.x % p.n_docs;
-  const long long off = p.dest_off[b];
-  const int len = (int)p.dest_len[b];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < kCsrWarps * len; t += blockDim.x) hw[t] = 0;
-  __syncthreads();
-  const long long src0 = ((long long)q * p.n_docs + b) * p.l_q;
-  const int32_t* a = p.argmax + src0;
-  const int chunk = ((p.l_q + kCsrWarps - 1) / kCsrWarps + 31) & ~31;
-  const int e0 = w * chunk, e1 = min(p.l_q, e0 + chunk);
-  int32_t* h = hw + w * len;
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const int key = __ldg(a + e);
-    if (key >= 0 && key < len) atomicAdd(&h[key], 1);
-  }
-  __syncthreads();
-  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;  // first slot of (q, b) per bucket
-  for (int r = threadIdx.x; r < len; r += blockDim.x) {
-    int run = base[r];
-#pragma unroll
-    for (int ww = 0; ww < kCsrWarps; ++ww) {
-      const int v = hw[ww * len + r];
-      hw[ww * len + r] = run;
-      run += v;
-    }
-  }
-  __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int e = e0; e < e1; e += 32) {
-    const int i = e + lane;
-    const bool valid = i < e1;
-    int key = valid ? __ldg(a + i) : -1;
-    const bool ok = valid && key >= 0 && key < len;
-    if (!ok) key = -1 - lane;  // distinct dummy keys never match real ones
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int rank = __popc(peers & lt_mask);
-    if (ok) p.col_idx[h[key] + rank] = (int32_t)(src0 + i);
-    __syncwarp();
-    if (ok && rank == 0) h[key] += __popc(peers);
-    __syncwarp();
-  }
-}
-
-// Warp-per-segment variants (used when every document has at most kCsrWarpLenMax rows): a
-// block holds kCsrWW segments, each warp its own shared-memory histogram / cursor array, so a
-// (q, b) segment needs no block barrier and all 4096 segments of C3 are resident in one wave
-// (the block-per-segment kernels above ran ~4 waves of tiny blocks).
-constexpr int kCsrWW = 8;
-constexpr int kCsrWarpLenMax = 1536;  // 8 warps x 1536 x 4 B = 48 KB per block
-
-__global__ void __launch_bounds__(32 * kCsrWW) csr_count_w_kernel(const CsrParams p, int hist_len) {
+// Shared memory: hw[W][H] per-warp counts (then cursors), T[H] CTA totals (read by the other
+// CTAs of the cluster), tot[H], bef[H] (document totals and lower-rank totals per bucket), then
+// tg[W][H] bytes of key-group tags for the placement.
+__global__ void __launch_bounds__(32 * kCsrMaxWarps) csr_doc_kernel(const CsrParams p) {
   extern __shared__ int32_t csr_sh[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long seg = (long long)blockIdx.x * kCsrWW + w;
-  if (seg >= (long long)p.n_q * p.n_docs) return;  // warp-uniform; no block barrier below
-  const int q = (int)(seg / p.n_docs), b = (int)(seg % p.n_docs);
+  __shared__ int32_t warp_sum[kCsrMaxWarps];
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.hist_len;
+  const uint32_t cl = cluster_nctarank(), rank = cluster_ctarank();
+  const int b = (int)(blockIdx.x / cl);
   const long long off = p.dest_off[b];
   const int len = (int)p.dest_len[b];
-  int32_t* hist = csr_sh + w * hist_len;
-  for (int t = lane; t < len; t += 32) hist[t] = 0;
-  __syncwarp();
-  const int32_t* a = p.argmax + seg * p.l_q;
-  for (int i = lane; i < p.l_q; i += 32) {
-    const int key = __ldg(a + i);
-    if (key >= 0 && key < len) atomicAdd(&hist[key], 1);
-  }
-  __syncwarp();
-  int32_t* out = p.cnt + (long long)q * p.n_dest + off;
-  for (int t = lane; t < len; t += 32) out[t] = hist[t];
-}
+  int32_t* T = csr_sh + nw * H;
+  int32_t* tot = T + H;
+  int32_t* bef = tot + H;
+  uint8_t* tg = reinterpret_cast<uint8_t*>(bef + H) + w * H;  // [W][H] group tags
+  for (int x = threadIdx.x; x < nw * H; x += blockDim.x) csr_sh[x] = 0;
+  __syncthreads();
 
-// Stable placement, one warp per (q, b) segment: 32 sources per step in source order; ranks of
-// equal keys inside the step from __match_any_sync, the bucket cursor advanced by the lowest lane
-// of each key group after everyone has read it.  Keys are prefetched 8 steps at a time.
-__global__ void __launch_bounds__(32 * kCsrWW) csr_place_w_kernel(const CsrParams p, int hist_len) {
-  extern __shared__ int32_t csr_sh[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long seg = (long long)blockIdx.x * kCsrWW + w;
-  if (seg >= (long long)p.n_q * p.n_docs) return;
-  const int q = (int)(seg / p.n_docs), b = (int)(seg % p.n_docs);
-  const long long off = p.dest_off[b];
-  const int len = (int)p.dest_len[b];
-  int32_t* cursor = csr_sh + w * hist_len;
-  const int32_t* base = p.cnt + (long long)q * p.n_dest + off;  // first slot of (q, b) per bucket
-  for (int t = lane; t < len; t += 32) cursor[t] = base[t];
-  __syncwarp();
-  const long long src0 = seg * p.l_q;
-  const int32_t* a = p.argmax + src0;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int e0 = 0; e0 < p.l_q; e0 += 32 * 8) {
+  const long long n_src = (long long)p.n_q * p.l_q;  // sources of this document (flat j)
+  const long long nwt = (long long)cl * nw;
+  const long long chunk = (((n_src + nwt - 1) / nwt) + 31) & ~31LL;
+  const long long j0 = min(n_src, (long long)(rank * nw + w) * chunk), j1 = min(n_src, j0 + chunk);
+  int32_t* h = csr_sh + w * H;
+
+  // 1. count (8 loads in flight per lane)
+  const int wrap = (p.n_docs - 1) * p.l_q;
+  SrcWalk wk;
+  if (j0 < j1) wk.init((uint32_t)(j0 + lane), p.lq_div, p.l_q, p.n_docs, b);
+  for (long long e0 = j0; e0 < j1; e0 += 32 * 8) {
     int keys[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int i = e0 + 32 * u + lane;
-      keys[u] = i < p.l_q ? __ldg(a + i) : -1;
+      keys[u] = (e0 + 32 * u + lane < j1) ? __ldg(p.argmax + wk.src) : -1;
+      wk.step32(p.l_q, wrap);
     }
 #pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (keys[u] >= 0 && keys[u] < len) atomicAdd(&h[keys[u]], 1);
+  }
+  __syncthreads();
+  // 2. exclusive prefix over this CTA's warps (in place) and the CTA totals
+  for (int t = threadIdx.x; t < len; t += blockDim.x) {
+    int run = 0;
+    for (int ww = 0; ww < nw; ++ww) {
+      const int v = csr_sh[ww * H + t];
+      csr_sh[ww * H + t] = run;
+      run += v;
+    }
+    T[t] = run;
+  }
+  // 3. cluster exchange: document totals and the totals of lower ranks, per bucket
+  if (cl > 1) {
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  } else {
+    __syncthreads();
+  }
+  const uint32_t t_addr = smem_u32(T);
+  const int per = (len + (int)blockDim.x - 1) / (int)blockDim.x;  // contiguous buckets per thread
+  const int t0 = min(len, (int)threadIdx.x * per), t1 = min(len, t0 + per);
+  int my_sum = 0;
+  for (int t = t0; t < t1; ++t) {
+    int s = 0, before = 0;
+    for (uint32_t r = 0; r < cl; ++r) {
+      const int v = (r == rank) ? T[t] : ld_cluster_s32(mapa_u32(t_addr + 4u * (uint32_t)t, r));
+      if (r < rank) before += v;
+      s += v;
+    }
+    tot[t] = s;
+    bef[t] = before;
+    my_sum += s;
+  }
+  if (cl > 1) cluster_arrive_release();  // done reading remote T (peers wait before exiting)
+  // block-wide exclusive scan of the per-thread sums
+  int x = my_sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  int wbase = 0;
+  for (int ww = 0; ww < w; ++ww) wbase += warp_sum[ww];
+  const long long doc_base = (long long)b * n_src;
+  int run = wbase + x - my_sum;  // exclusive prefix of this thread's first bucket within the document
+  for (int t = t0; t < t1; ++t) {
+    const int base = (int)doc_base + run;
+    if (rank == 0) p.row_ptr[off + t] = base;
+    const int c = base + bef[t];
+    for (int ww = 0; ww < nw; ++ww) csr_sh[ww * H + t] += c;
+    run += tot[t];
+  }
+  if (rank == 0 && threadIdx.x == 0 && b == p.n_docs - 1) p.row_ptr[p.n_dest] = (int32_t)(doc_base + n_src);
+  __syncthreads();
+
+  // 4. stable placement, one warp per range in source order
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (j0 < j1) wk.init((uint32_t)(j0 + lane), p.lq_div, p.l_q, p.n_docs, b);
+  for (long long e0 = j0; e0 < j1; e0 += 32 * 8) {
+    int keys[8], srcs[8];
+    unsigned pm[8];
+#pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int i = e0 + 32 * u + lane;
-      if (e0 + 32 * u >= p.l_q) break;  // warp-uniform
-      int key = keys[u];
-      const bool ok = i < p.l_q && key >= 0 && key < len;
-      if (!ok) key = -1 - lane;  // distinct dummy keys never match real ones
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const int rank = __popc(peers & lt_mask);
-      int slot = 0;
-      if (ok) slot = cursor[key] + rank;
+      keys[u] = (e0 + 32 * u + lane < j1) ? __ldg(p.argmax + wk.src) : -1;
+      srcs[u] = wk.src;
+      wk.step32(p.l_q, wrap);
+    }
+    // equal-key peer masks of the 8 steps.  A per-warp byte tag array names every key group by
+    // one of its lanes (each lane writes its lane id at tg[key]; the surviving writer is the
+    // group's id), so the masks need 5 ballots on that id instead of one per key bit (or
+    // MATCH.ANY, whose issue cost serialised the loop); the ballots of the 8 steps interleave.
+    int gid[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = keys[u] >= 0 && keys[u] < len;
+      if (ok) tg[keys[u]] = (uint8_t)lane;
       __syncwarp();
-      if (ok) {
-        p.col_idx[slot] = (int32_t)(src0 + i);
-        if (rank == 0) cursor[key] += __popc(peers);
+      gid[u] = ok ? (int)tg[keys[u]] : 32 + lane;
+      __syncwarp();
+      pm[u] = __ballot_sync(0xffffffffu, ok);
+    }
+#pragma unroll
+    for (int bit = 0; bit < 5; ++bit) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool set = (gid[u] >> bit) & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, set);
+        pm[u] &= set ? bal : ~bal;
       }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (gid[u] >= 32) pm[u] = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (e0 + 32 * u >= j1) break;  // warp-uniform
+      const bool ok = pm[u] != 0;
+      const int rk = __popc(pm[u] & lt_mask);
+      int v = 0;
+      if (ok && rk == 0) {  // the lowest lane of each key group advances the bucket cursor
+        v = h[keys[u]];
+        h[keys[u]] = v + __popc(pm[u]);
+      }
+      v = __shfl_sync(0xffffffffu, v, ok ? __ffs(pm[u]) - 1 : lane);
+      if (ok) p.col_idx[v + rk] = srcs[u];
       __syncwarp();
     }
+  }
+  if (cl > 1) cluster_wait_acquire();  // keep T alive until every peer has read it
+}
+
+// ---------------------------------------------------------------- general path (radix sort)
+// keys[s] = global destination row of source s (n_dest for an out-of-range argmax: sorts last,
+// outside every row), vals[s] = s.
+__global__ void __launch_bounds__(256) csr_sort_keys_kernel(const CsrParams p, int32_t* keys, int32_t* vals) {
+  const long long n = (long long)p.n_q * p.n_docs * p.l_q;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n; s += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)((s / p.l_q) % p.n_docs);
+    const int a = p.argmax[s];
+    const long long len = p.dest_len[b];
+    keys[s] = (a >= 0 && a < len) ? (int32_t)(p.dest_off[b] + a) : (int32_t)p.n_dest;
+    vals[s] = (int32_t)s;
+  }
+}
+
+// row_ptr[r] = first position of a key >= r in the sorted keys (r = 0 .. n_dest).
+__global__ void __launch_bounds__(256) csr_sort_rowptr_kernel(const int32_t* sorted_keys, long long n, long long n_dest,
+                                                              int32_t* row_ptr) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= n_dest;
+       r += (long long)gridDim.x * blockDim.x) {
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (sorted_keys[mid] < r)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    row_ptr[r] = (int32_t)lo;
   }
 }
 

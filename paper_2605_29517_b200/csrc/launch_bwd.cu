@@ -5,6 +5,8 @@
 #include <mutex>
 #include <type_traits>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "csr.cuh"
 #include "grad.cuh"
 #include "host.h"
@@ -75,20 +77,26 @@ static bool launch_grad_query_vec(const T* D, const mxs::GradParams& p, long lon
 
 extern "C" {
 
-size_t mxs_csr_workspace_bytes(int64_t n_q, int64_t n_dest) { return (size_t)(n_q * n_dest) * sizeof(int32_t); }
+// The CSR build needs no caller workspace any more (csr_doc_kernel keeps its histograms in shared
+// memory; the radix-sort path allocates stream-ordered scratch itself).  The entry point and the
+// ws arguments stay for ABI stability.
+size_t mxs_csr_workspace_bytes(int64_t n_q, int64_t n_dest) {
+  (void)n_q;
+  (void)n_dest;
+  return 0;
+}
 
 int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, int64_t l_q, const int64_t* dest_off,
                           const int64_t* dest_len, int64_t n_dest, int64_t max_dest_len, int32_t* row_ptr,
                           int32_t* col_idx, void* ws, size_t ws_bytes, void* stream) {
-  if (!argmax || !dest_off || !dest_len || !row_ptr || !col_idx || !ws)
+  (void)ws;
+  (void)ws_bytes;
+  if (!argmax || !dest_off || !dest_len || !row_ptr || !col_idx)
     return fail(MXS_INVALID_ARGUMENT, "mxs_build_inverse_csr: null pointer");
-  if (n_q < 1 || n_docs < 1 || l_q < 1 || n_dest < 1) return fail(MXS_SHAPE_MISMATCH, "mxs_build_inverse_csr: bad shape");
-  if (n_q * n_docs * l_q >= (1LL << 31) || n_dest >= (1LL << 31))
+  if (n_q < 1 || n_docs < 1 || l_q < 1 || n_dest < 1 || max_dest_len < 1)
+    return fail(MXS_SHAPE_MISMATCH, "mxs_build_inverse_csr: bad shape");
+  if (n_q * n_docs * l_q >= (1LL << 31) || n_dest >= (1LL << 31) - 1)
     return fail(MXS_UNSUPPORTED, "mxs_build_inverse_csr: more than 2^31 sources or destinations");
-  if (ws_bytes < mxs_csr_workspace_bytes(n_q, n_dest))
-    return fail(MXS_INVALID_ARGUMENT, "mxs_build_inverse_csr: workspace too small");
-  const size_t hist_bytes = (size_t)max_dest_len * sizeof(int32_t);
-  if (hist_bytes > 200 * 1024) return fail(MXS_UNSUPPORTED, "document longer than %lld rows", (long long)(200 * 256));
   mxs::CsrParams p;
   p.argmax = argmax;
   p.dest_off = (const long long*)dest_off;
@@ -97,41 +105,64 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
   p.n_docs = (int)n_docs;
   p.l_q = (int)l_q;
   p.n_dest = n_dest;
-  p.cnt = (int32_t*)ws;
   p.row_ptr = row_ptr;
   p.col_idx = col_idx;
   cudaStream_t st = (cudaStream_t)stream;
   int s;
-  if ((s = ensure_smem((const void*)mxs::csr_count_kernel, 200 * 1024)) != MXS_OK ||
-      (s = ensure_smem((const void*)mxs::csr_place_kernel, 200 * 1024)) != MXS_OK ||
-      (s = ensure_smem((const void*)mxs::csr_place_v2_kernel, 200 * 1024)) != MXS_OK ||
-      (s = ensure_smem((const void*)mxs::csr_count_w_kernel, 64 * 1024)) != MXS_OK ||
-      (s = ensure_smem((const void*)mxs::csr_place_w_kernel, 64 * 1024)) != MXS_OK)
-    return s;
-  const unsigned segs = (unsigned)(n_q * n_docs);
-  // rows that belong to no document (never the case for padded / packed layouts) stay zero
-  if (cudaMemsetAsync(ws, 0, mxs_csr_workspace_bytes(n_q, n_dest), st) != cudaSuccess)
-    return fail(MXS_CUDA_ERROR, "memset");
-  if (cudaMemsetAsync(row_ptr, 0, sizeof(int32_t) * (size_t)(n_dest + 1), st) != cudaSuccess)
-    return fail(MXS_CUDA_ERROR, "memset");
-  const bool warp_seg = max_dest_len <= mxs::kCsrWarpLenMax && !getenv("MXS_CSR_BLOCK");
-  const int hist_len = (int)((max_dest_len + 3) & ~3LL);
-  const size_t wsh = (size_t)mxs::kCsrWW * hist_len * sizeof(int32_t);
-  const unsigned wblocks = (unsigned)((segs + mxs::kCsrWW - 1) / mxs::kCsrWW);
-  if (warp_seg)
-    mxs::csr_count_w_kernel<<<wblocks, 32 * mxs::kCsrWW, wsh, st>>>(p, hist_len);
-  else
-    mxs::csr_count_kernel<<<segs, 256, hist_bytes, st>>>(p);
-  if ((s = check_launch("csr_count_kernel")) != MXS_OK) return s;
-  mxs::csr_scan_kernel<<<(unsigned)n_docs, 1024, 0, st>>>(p);
-  if ((s = check_launch("csr_scan_kernel")) != MXS_OK) return s;
-  if (warp_seg)
-    mxs::csr_place_w_kernel<<<wblocks, 32 * mxs::kCsrWW, wsh, st>>>(p, hist_len);
-  else if (hist_bytes * mxs::kCsrWarps <= 200 * 1024)
-    mxs::csr_place_v2_kernel<<<segs, 32 * mxs::kCsrWarps, hist_bytes * mxs::kCsrWarps, st>>>(p);
-  else
-    mxs::csr_place_kernel<<<segs, 256, hist_bytes, st>>>(p);
-  return check_launch("csr_place_kernel");
+  // shared-memory plan of csr_doc_kernel: (W + 3) rows of H int32 + W rows of H bytes per CTA
+  constexpr size_t kSmemMax = 227 * 1024 - 256;
+  const long long H = (max_dest_len + 3) & ~3LL;
+  const long long w_cap = ((long long)(kSmemMax / (size_t)H) - 12) / 5;
+  if (w_cap >= 1 && !env_is("MXS_CSR_IMPL", "sort")) {
+    const long long n_src = n_q * l_q;
+    const long long per_warp = std::max(32, env_int("MXS_CSR_SRC_PER_WARP", 1024));
+    const long long nwt = std::min<long long>(8 * mxs::kCsrMaxWarps, std::max(1LL, (n_src + per_warp - 1) / per_warp));
+    const int W = (int)std::min<long long>(std::min<long long>(mxs::kCsrMaxWarps, w_cap), nwt);
+    const int CL = (int)std::min<long long>(8, (nwt + W - 1) / W);
+    p.hist_len = (int)H;
+    p.lq_div = mxs::make_fastdiv((uint32_t)l_q);
+    const size_t smem = (size_t)(W + 3) * (size_t)H * sizeof(int32_t) + (size_t)W * (size_t)H;
+    if ((s = ensure_smem((const void*)mxs::csr_doc_kernel, smem)) != MXS_OK) return s;
+    void* args[] = {&p};
+    return launch_cluster((const void*)mxs::csr_doc_kernel, n_docs * CL, CL, 32 * W, smem, st, args, "csr_doc_kernel");
+  }
+  // general path: stable radix sort of (destination row, source) pairs
+  const long long n = n_q * n_docs * l_q;
+  int end_bit = 1;
+  while (end_bit < 31 && (1LL << end_bit) <= n_dest) ++end_bit;
+  size_t temp = 0;
+  cub::DoubleBuffer<int32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
+  if (cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, 0, end_bit, st) != cudaSuccess)
+    return fail(MXS_CUDA_ERROR, "csr radix sort: temp query failed");
+  const size_t arr = ((size_t)n * sizeof(int32_t) + 255) & ~(size_t)255;
+  char* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, 3 * arr + temp, st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MXS_CUDA_ERROR, "csr radix sort: cannot allocate %zu bytes of scratch", 3 * arr + temp);
+  }
+  int32_t* k0 = (int32_t*)buf;
+  int32_t* k1 = (int32_t*)(buf + arr);
+  int32_t* v0 = (int32_t*)(buf + 2 * arr);
+  const int nsm = sm_count();
+  const unsigned blocks = (unsigned)std::max(1LL, std::min<long long>((n + 255) / 256, (long long)nsm * 8));
+  mxs::csr_sort_keys_kernel<<<blocks, 256, 0, st>>>(p, k0, v0);
+  s = check_launch("csr_sort_keys_kernel");
+  if (s == MXS_OK) {
+    // values ping-pong between v0 and col_idx; keys between k0 and k1
+    cub::DoubleBuffer<int32_t> keys(k0, k1), vals(v0, col_idx);
+    if (cub::DeviceRadixSort::SortPairs(buf + 3 * arr, temp, keys, vals, (int)n, 0, end_bit, st) != cudaSuccess)
+      s = fail(MXS_CUDA_ERROR, "csr radix sort failed");
+    if (s == MXS_OK && vals.Current() != col_idx &&
+        cudaMemcpyAsync(col_idx, vals.Current(), (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      s = fail(MXS_CUDA_ERROR, "csr radix sort: copy");
+    if (s == MXS_OK) {
+      const unsigned rb = (unsigned)std::max(1LL, std::min<long long>((n_dest + 256) / 256, (long long)nsm * 8));
+      mxs::csr_sort_rowptr_kernel<<<rb, 256, 0, st>>>(keys.Current(), n, n_dest, row_ptr);
+      s = check_launch("csr_sort_rowptr_kernel");
+    }
+  }
+  cudaFreeAsync(buf, st);
+  return s;
 }
 
 int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx, int64_t n_dest, const float* g,

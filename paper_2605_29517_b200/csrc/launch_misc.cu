@@ -156,11 +156,14 @@ int mxs_chamfer_nn(const float* A, const float* a_norms, int64_t n, const float*
                    int64_t dim, float* best, int32_t* idx, void* stream) {
   if (!A || !a_norms || !B || !b_norms || !best || !idx) return fail(MXS_INVALID_ARGUMENT, "mxs_chamfer_nn: null");
   if (n < 1 || m < 1) return fail(MXS_SHAPE_MISMATCH, "point set must hold at least one point");
-  if (dim < 1 || dim > mxs::kChDimMax) return fail(MXS_UNSUPPORTED, "mxs_chamfer_nn: dim %lld outside [1, 16]", (long long)dim);
+  if (dim < 1 || dim > 8192) return fail(MXS_UNSUPPORTED, "mxs_chamfer_nn: dim %lld outside [1, 8192]", (long long)dim);
   if (m >= (1LL << 31)) return fail(MXS_UNSUPPORTED, "mxs_chamfer_nn: more than 2^31 points");
   const long long blocks = (n + mxs::kChThreads - 1) / mxs::kChThreads;
   cudaStream_t st = (cudaStream_t)stream;
-  if (dim == 3)
+  if (dim > mxs::kChDimMax)
+    mxs::chamfer_nn_any_kernel<<<(unsigned)blocks, mxs::kChThreads, 0, st>>>(A, a_norms, n, B, b_norms, m, (int)dim,
+                                                                             best, idx);
+  else if (dim == 3)
     mxs::chamfer_nn_kernel<3><<<(unsigned)blocks, mxs::kChThreads, 0, st>>>(A, a_norms, n, B, b_norms, m, 3, best, idx);
   else
     mxs::chamfer_nn_kernel<0><<<(unsigned)blocks, mxs::kChThreads, 0, st>>>(A, a_norms, n, B, b_norms, m, (int)dim,

@@ -71,7 +71,7 @@ def test_argument_validation_maps_to_reference_errors(lib):
 
 
 def test_workspace_sizes(lib):
-    assert lib.mxs_csr_workspace_bytes(64, 65536) == 64 * 65536 * 4
+    assert lib.mxs_csr_workspace_bytes(64, 65536) == 0  # histograms live in shared memory / sort scratch
     assert lib.mxs_topk_workspace_bytes(10000, 20) == 0  # one 16384-element selection slice (k <= 128)
     assert lib.mxs_topk_workspace_bytes(20000, 20) == 2 * 20 * 16
     assert lib.mxs_topk_workspace_bytes(10000, 200) == 3 * 200 * 16  # 4096-element bitonic slices

@@ -86,3 +86,53 @@ def test_large_cloud_against_f64_oracle():
     assert torch.allclose(got, best, rtol=1e-4, atol=1e-6)
     d_p, d_s = mx.chamfer_backward(p, s, a1, a2)
     assert d_p.shape == (20_000, 3) and d_s.shape == (30_000, 3)
+
+
+def _numpy_nearest(a, b):
+    """The reference's float32 arithmetic (maxsim/kernels.py:29-66 dot_block / sq_norms /
+    sq_dist_block, fold_extreme strict <) restated with numpy on the whole pair grid."""
+    def norms(x):
+        out = x[:, 0] * x[:, 0]
+        for k in range(1, x.shape[1]):
+            out = out + x[:, k] * x[:, k]
+        return out
+
+    dot = a[:, 0, None] * b[None, :, 0]
+    for k in range(1, a.shape[1]):
+        dot = dot + a[:, k, None] * b[None, :, k]
+    d = dot * np.float32(-2.0) + norms(a)[:, None] + norms(b)[None, :]
+    return d.min(axis=1), d.argmin(axis=1)
+
+
+@gpu
+@pytest.mark.parametrize("dim", [3, 17, 40])
+def test_any_dimension_bit_exact(dim):
+    """Chamfer is dimension-generic in the reference: wide embeddings (dim > 16) take the
+    shared-memory-tiled kernel with the same fold, bit-identical distances and argmins."""
+    rng = np.random.default_rng(dim)
+    p = rng.standard_normal((301, dim)).astype(np.float32)
+    s = rng.standard_normal((203, dim)).astype(np.float32)
+    s[7] = p[11]  # an exact match and a duplicate (tie -> lowest index)
+    s[9] = p[11]
+    cd, a1, a2 = mx.chamfer_forward(p, s)
+    b1, i1 = _numpy_nearest(p, s)
+    b2, i2 = _numpy_nearest(s, p)
+    assert np.array_equal(a1.cpu().numpy(), i1) and np.array_equal(a2.cpu().numpy(), i2)
+    ref = float(np.add.accumulate(b1, dtype=np.float64)[-1]) / 301 + float(np.add.accumulate(b2, dtype=np.float64)[-1]) / 203
+    assert cd == ref
+    d_p, d_s = mx.chamfer_backward(p, s, a1, a2)
+    r_p, r_s = mx.dense_chamfer_backward(p, s, a1, a2)
+    assert torch.allclose(d_p, r_p, rtol=1e-12, atol=0) and torch.allclose(d_s, r_s, rtol=1e-12, atol=0)
+
+
+@gpu
+def test_clouds_beyond_shared_memory_histograms():
+    """More than 51,200 points per cloud: the backward's inverse CSR takes the
+    radix-sort path and stays equal to the dense float64 scatter."""
+    rng = np.random.default_rng(77)
+    p = rng.standard_normal((60_000, 3)).astype(np.float32)
+    s = rng.standard_normal((55_000, 3)).astype(np.float32)
+    cd, a1, a2 = mx.chamfer_forward(p, s)
+    d_p, d_s = mx.chamfer_backward(p, s, a1, a2, upstream=1.3)
+    r_p, r_s = mx.dense_chamfer_backward(p, s, a1, a2, upstream=1.3)
+    assert torch.allclose(d_p, r_p, rtol=1e-12, atol=1e-300) and torch.allclose(d_s, r_s, rtol=1e-12, atol=1e-300)

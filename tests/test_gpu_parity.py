@@ -382,6 +382,43 @@ def test_csr_c3_scale_bitwise():
     assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
 
 
+@pytest.mark.parametrize("impl,per_warp", [("doc", "32"), ("doc", "1024"), ("doc", "100000"), ("sort", None)])
+def test_csr_every_path_bitwise(monkeypatch, impl, per_warp):
+    """Both CSR builders (cluster-per-document counting sort with 1..8 CTAs per cluster and 1..16
+    warps per CTA, and the radix-sort path) against the oracle's stable argsort, on random,
+    all-hot, packed and long-document maps (the reference's long_doc regime, L_d >= 2048)."""
+    if impl == "sort":
+        monkeypatch.setenv("MXS_CSR_IMPL", "sort")
+    if per_warp:
+        monkeypatch.setenv("MXS_CSR_SRC_PER_WARP", per_warp)
+    rng = np.random.default_rng(31)
+    cases = [(3, 5, 300, 77), (1, 1, 5000, 2048), (2, 3, 700, 4096), (64, 2, 1024, 1024), (1, 2, 40, 9000)]
+    for trial, (n_q, b, l_q, L) in enumerate(cases):
+        lens = rng.integers(1, L + 1, b)
+        lens[0] = L
+        idx = np.stack([np.stack([rng.integers(0, lens[j], l_q) for j in range(b)]) for _ in range(n_q)])
+        if trial % 2:
+            idx[..., : l_q // 3] = 0  # a hot bucket inside every segment
+        packed = trial % 2 == 1
+        am = mx.ArgmaxMap(idx.astype(np.int32), lens, padded_len=None if packed else L)
+        rp, ci = mx.build_inverse_csr(am).to_numpy()
+        orp, oci = orc.build_inverse_csr(idx, lens, None if packed else L)
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci), (impl, per_warp, trial)
+
+
+def test_csr_destination_beyond_shared_memory():
+    """A single destination block far longer than a shared-memory histogram (Chamfer clouds of
+    more than 51,200 points) takes the radix-sort path, still bit-identical."""
+    rng = np.random.default_rng(32)
+    n_src, n_dest = 70_000, 60_000
+    idx = rng.integers(0, n_dest, (1, 1, n_src)).astype(np.int32)
+    idx[0, 0, ::7] = 12345
+    am = mx.ArgmaxMap(idx, [n_dest], padded_len=n_dest)
+    rp, ci = mx.build_inverse_csr(am).to_numpy()
+    orp, oci = orc.build_inverse_csr(idx, [n_dest], n_dest)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+
+
 def test_backward_golden():
     g = golden("backward")
     docs = mx.DocBatch.from_dense(g["D"], g["valid_lens"])
