@@ -28,7 +28,9 @@ class PointSet:
     __slots__ = ("data", "n", "dim")
 
     def __init__(self, points):
-        src = points.data if isinstance(points, PointSet) else points
+        # our PointSet, or the reference's (numpy .data with .n / .dim) -- duck-typed
+        src = points.data if isinstance(points, PointSet) or (hasattr(points, "data") and hasattr(points, "n")) \
+            else points
         if isinstance(src, torch.Tensor):
             t = src.detach().to(torch.float32)
         else:
