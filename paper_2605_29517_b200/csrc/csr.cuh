@@ -13,8 +13,8 @@
 //      (exclusive scan over the document's rows, one block scan) + the totals of lower ranks
 //      -> each warp's first slot in every bucket.  Rank 0 writes row_ptr.
 //   4. place:  every warp walks its range in source order, 32 keys per step; equal keys inside a
-//      step are grouped through a byte tag per bucket + 5 ballots (8 steps interleaved), ranked
-//      by lane, and the lowest lane of each group advances the bucket cursor.
+//      step find each other through a per-bucket lane-mask word (atomicOr, read back), are
+//      ranked by lane, and the lowest lane of each group advances the bucket cursor.
 // The CSR is therefore the stable counting sort the reference computes, with no atomics on
 // global memory and one pass over argmax for the count plus one (L2-resident) for the placement.
 //
@@ -97,7 +97,7 @@ constexpr int kCsrMaxWarps = 16;
 
 // Shared memory: hw[W][H] per-warp counts (then cursors), T[H] CTA totals (read by the other
 // CTAs of the cluster), tot[H], bef[H] (document totals and lower-rank totals per bucket), then
-// tg[W][H] bytes of key-group tags for the placement.
+// mk[W][H] per-warp key-group lane masks for the placement.
 __global__ void __launch_bounds__(32 * kCsrMaxWarps) csr_doc_kernel(const CsrParams p) {
   extern __shared__ int32_t csr_sh[];
   __shared__ int32_t warp_sum[kCsrMaxWarps];
@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(32 * kCsrMaxWarps) csr_doc_kernel(const CsrPar
   int32_t* T = csr_sh + nw * H;
   int32_t* tot = T + H;
   int32_t* bef = tot + H;
-  uint8_t* tg = reinterpret_cast<uint8_t*>(bef + H) + w * H;  // [W][H] group tags
+  uint32_t* mk = reinterpret_cast<uint32_t*>(bef + H) + w * H;  // [W][H] per-step key-group lane masks
   for (int x = threadIdx.x; x < nw * H; x += blockDim.x) csr_sh[x] = 0;
+  for (int x = threadIdx.x; x < nw * H; x += blockDim.x) reinterpret_cast<uint32_t*>(bef + H)[x] = 0u;
   __syncthreads();
 
   const long long n_src = (long long)p.n_q * p.l_q;  // sources of this document (flat j)
@@ -197,50 +198,33 @@ __global__ void __launch_bounds__(32 * kCsrMaxWarps) csr_doc_kernel(const CsrPar
   if (j0 < j1) wk.init((uint32_t)(j0 + lane), p.lq_div, p.l_q, p.n_docs, b);
   for (long long e0 = j0; e0 < j1; e0 += 32 * 8) {
     int keys[8], srcs[8];
-    unsigned pm[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       keys[u] = (e0 + 32 * u + lane < j1) ? __ldg(p.argmax + wk.src) : -1;
       srcs[u] = wk.src;
       wk.step32(p.l_q, wrap);
     }
-    // equal-key peer masks of the 8 steps.  A per-warp byte tag array names every key group by
-    // one of its lanes (each lane writes its lane id at tg[key]; the surviving writer is the
-    // group's id), so the masks need 5 ballots on that id instead of one per key bit (or
-    // MATCH.ANY, whose issue cost serialised the loop); the ballots of the 8 steps interleave.
-    int gid[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool ok = keys[u] >= 0 && keys[u] < len;
-      if (ok) tg[keys[u]] = (uint8_t)lane;
-      __syncwarp();
-      gid[u] = ok ? (int)tg[keys[u]] : 32 + lane;
-      __syncwarp();
-      pm[u] = __ballot_sync(0xffffffffu, ok);
-    }
-#pragma unroll
-    for (int bit = 0; bit < 5; ++bit) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool set = (gid[u] >> bit) & 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, set);
-        pm[u] &= set ? bal : ~bal;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (gid[u] >= 32) pm[u] = 0;
+    // stable placement of the 8 steps in order.  Equal keys of a step find each other through a
+    // per-warp lane-mask word per bucket: every lane ORs its bit in (atomic, so the shared word
+    // has no unordered writers), reads the group mask back, and the group's lowest lane advances
+    // the cursor and clears the word for the next step -- no MATCH.ANY, no ballot per key bit.
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (e0 + 32 * u >= j1) break;  // warp-uniform
-      const bool ok = pm[u] != 0;
-      const int rk = __popc(pm[u] & lt_mask);
+      const int key = keys[u];
+      const bool ok = key >= 0 && key < len;
+      if (ok) atomicOr(&mk[key], 1u << lane);
+      __syncwarp();
+      const uint32_t pm = ok ? mk[key] : 0u;
+      __syncwarp();
+      const int rk = __popc(pm & lt_mask);
       int v = 0;
       if (ok && rk == 0) {  // the lowest lane of each key group advances the bucket cursor
-        v = h[keys[u]];
-        h[keys[u]] = v + __popc(pm[u]);
+        v = h[key];
+        h[key] = v + __popc(pm);
+        mk[key] = 0u;
       }
-      v = __shfl_sync(0xffffffffu, v, ok ? __ffs(pm[u]) - 1 : lane);
+      v = __shfl_sync(0xffffffffu, v, ok ? __ffs(pm) - 1 : lane);
       if (ok) p.col_idx[v + rk] = srcs[u];
       __syncwarp();
     }

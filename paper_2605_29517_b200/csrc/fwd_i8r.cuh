@@ -38,7 +38,8 @@ constexpr int kR8PartBufs = 4;  // per-document partial-maximum buffers in fligh
 
 struct R8SmemHeader {
   uint32_t pcnt[kR8PartBufs][4];  // sets (warps) of a quadrant that have published doc partials
-  uint32_t pgen[kR8PartBufs][4];  // documents combined out of this buffer so far
+  uint64_t pdone[kR8PartBufs][4];  // all lanes of the three set warps of a quadrant published
+  uint64_t pfree[kR8PartBufs][4];  // the combiner warp has read the buffer (it may be refilled)
   uint64_t full[8];
   uint64_t empty[8];
   uint64_t tfull[kR8Sets];
@@ -123,8 +124,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   }
   if (threadIdx.x < kR8PartBufs * 4) {
     (&hdr->pcnt[0][0])[threadIdx.x] = 0u;
-    (&hdr->pgen[0][0])[threadIdx.x] = 0u;
+    mbar_init(&hdr->pdone[0][0] + threadIdx.x, 32 * kR8Sets);
+    mbar_init(&hdr->pfree[0][0] + threadIdx.x, 32);
   }
+  if (threadIdx.x == 0) fence_mbar_init();
   if (warp == 1) tmem_alloc(&hdr->tmem_base, 512);
   if constexpr (KIND == TcKind::I8) {
     fill_bias_tile(sBias, (int)threadIdx.x, kR8Threads);
@@ -383,45 +386,39 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         }
         ++sc_n;
       }
-      // ---- combine the three sets' partial maxima of this document without a barrier: every warp
-      // publishes its partials into the document's buffer and counts itself in; the last of the
-      // three warps of a quadrant (one per set) max-combines the quadrant's rows and writes them.
-      // A set can run several documents ahead of another (small documents), so a buffer is only
-      // re-filled once its previous document has been combined (generation check, rarely waits).
+      // ---- combine the three sets' partial maxima of this document without waiting for the
+      // slowest set: every warp publishes its partials into the document's buffer (all lanes
+      // arrive on pdone) and counts itself in; the last of the three warps of a quadrant (one per
+      // set) max-combines the quadrant's rows and writes them.  A set can run several documents
+      // ahead of another (small documents), so a buffer is refilled only after its previous
+      // document's combiner released it (pfree; rarely waits).
       const uint32_t pb = ndoc % kR8PartBufs, gen = ndoc / kR8PartBufs;
-      volatile uint32_t* pgen = &hdr->pgen[pb][quad];
-      while (*pgen != gen) {
-      }
+      if (gen > 0) mbar_wait(&hdr->pfree[pb][quad], (gen - 1u) & 1u);
       float* buf = sPart + (size_t)pb * kR8Sets * 4 * 128;
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) buf[(set * 4 + mb) * 128 + row_local] = part[mb];
-      __threadfence_block();
-      __syncwarp();
+      mbar_arrive(&hdr->pdone[pb][quad]);
       uint32_t arrived = 0;
       if (lane == 0) arrived = atomicAdd(&hdr->pcnt[pb][quad], 1u);
       arrived = __shfl_sync(0xffffffffu, arrived, 0);
       if (arrived == kR8Sets - 1) {
-        __threadfence_block();
-        const volatile float* vb = buf;
+        mbar_wait(&hdr->pdone[pb][quad], gen & 1u);  // complete: the other two arrived before counting in
         const long long obase = ((long long)q * p.n_docs + b) * p.l_q;
         const uint32_t sb = ndoc & 1u;
         if (fuse) mbar_wait_cl<CL>(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
         for (int mb = 0; mb < qbv; ++mb) {
           const int row = (g * p.qb + mb) * kTileRows + row_local;
-          const float m = fmaxf(fmaxf(vb[(0 * 4 + mb) * 128 + row_local], vb[(1 * 4 + mb) * 128 + row_local]),
-                                vb[(2 * 4 + mb) * 128 + row_local]);
+          const float m = fmaxf(fmaxf(buf[(0 * 4 + mb) * 128 + row_local], buf[(1 * 4 + mb) * 128 + row_local]),
+                                buf[(2 * 4 + mb) * 128 + row_local]);
           if (row < p.l_q) {
             if (p.rowmax) p.rowmax[obase + row] = m;
             if (fuse) st_rank0_f32<CL>(sSum + sb * p.sum_rows + row, m);
           }
         }
         if (fuse) mbar_arrive_rank<CL>(&hdr->sready[sb], 0u);
+        if (lane == 0) hdr->pcnt[pb][quad] = 0u;
         __syncwarp();
-        if (lane == 0) {
-          hdr->pcnt[pb][quad] = 0u;
-          __threadfence_block();
-          *pgen = gen + 1u;
-        }
+        mbar_arrive(&hdr->pfree[pb][quad]);  // every lane: its reads of the buffer are done
       }
       ++ndoc;
     }

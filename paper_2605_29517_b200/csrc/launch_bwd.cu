@@ -109,19 +109,19 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
   p.col_idx = col_idx;
   cudaStream_t st = (cudaStream_t)stream;
   int s;
-  // shared-memory plan of csr_doc_kernel: (W + 3) rows of H int32 + W rows of H bytes per CTA
+  // shared-memory plan of csr_doc_kernel: (2W + 3) rows of H 32-bit words per CTA
   constexpr size_t kSmemMax = 227 * 1024 - 256;
   const long long H = (max_dest_len + 3) & ~3LL;
-  const long long w_cap = ((long long)(kSmemMax / (size_t)H) - 12) / 5;
+  const long long w_cap = ((long long)(kSmemMax / (4 * (size_t)H)) - 3) / 2;
   if (w_cap >= 1 && !env_is("MXS_CSR_IMPL", "sort")) {
     const long long n_src = n_q * l_q;
-    const long long per_warp = std::max(32, env_int("MXS_CSR_SRC_PER_WARP", 1024));
+    const long long per_warp = std::max(32, env_int("MXS_CSR_SRC_PER_WARP", 2048));
     const long long nwt = std::min<long long>(8 * mxs::kCsrMaxWarps, std::max(1LL, (n_src + per_warp - 1) / per_warp));
-    const int W = (int)std::min<long long>(std::min<long long>(mxs::kCsrMaxWarps, w_cap), nwt);
+    const int W = (int)std::min<long long>(std::min<long long>(env_int("MXS_CSR_WARPS", mxs::kCsrMaxWarps), w_cap), nwt);
     const int CL = (int)std::min<long long>(8, (nwt + W - 1) / W);
     p.hist_len = (int)H;
     p.lq_div = mxs::make_fastdiv((uint32_t)l_q);
-    const size_t smem = (size_t)(W + 3) * (size_t)H * sizeof(int32_t) + (size_t)W * (size_t)H;
+    const size_t smem = (size_t)(2 * W + 3) * (size_t)H * sizeof(int32_t);
     if ((s = ensure_smem((const void*)mxs::csr_doc_kernel, smem)) != MXS_OK) return s;
     void* args[] = {&p};
     return launch_cluster((const void*)mxs::csr_doc_kernel, n_docs * CL, CL, 32 * W, smem, st, args, "csr_doc_kernel");

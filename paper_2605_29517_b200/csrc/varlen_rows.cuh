@@ -365,8 +365,7 @@ MXS_DEV void vr_scan(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh,
     sh->ha[set][pb][pidx] = (int16_t)ha;
     sh->tm[set][pb][pidx] = m;
     sh->ta[set][pb][pidx] = (int16_t)a;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&hdr->pfull[set][pb]);
+    mbar_arrive(&hdr->pfull[set][pb]);  // every lane (release of its own stores)
   }
 }
 
@@ -456,8 +455,7 @@ MXS_DEV void vr_merge(const VarlenRowsParams& p, VrSmemHeader* hdr, VrShared* sh
     else
       vr_fold_ranges<C, false, FUSED>(f, sh->hm[set][pb], sh->ha[set][pb], sh->tm[set][pb], sh->ta[set][pb], w, d_first,
                                ntok, row, p, rbase);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&hdr->pempty[set][pb]);
+    mbar_arrive(&hdr->pempty[set][pb]);  // every lane (its reads are done)
     if (!vr_bit(w, 0) && (f.thm > cm || cd < 0)) {  // the tile head continues the carried document
       cm = f.thm;
       ca = p0 + f.tha;
@@ -517,8 +515,8 @@ __global__ void __launch_bounds__(kVrThreads, 1)
     }
     for (int s = 0; s < 2; ++s)
       for (int b = 0; b < kVrPieceBufs; ++b) {
-        mbar_init(&hdr->pfull[s][b], (uint32_t)n_active);
-        mbar_init(&hdr->pempty[s][b], (uint32_t)n_merge);
+        mbar_init(&hdr->pfull[s][b], 32u * (uint32_t)n_active);  // all lanes of the scan warps
+        mbar_init(&hdr->pempty[s][b], 32u * (uint32_t)n_merge);  // all lanes of the merge warps
       }
     fence_mbar_init();
   }
