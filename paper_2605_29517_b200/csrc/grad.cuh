@@ -22,7 +22,15 @@ struct GradParams {
   const int32_t* argmax;       // [n_q, n_docs, l_q]
   const long long* doc_row_off;  // [n_docs] first row of each document in D
   float* dQ;                   // [n_q, l_q, dim]
+  // debug ownership ledger (MXS_DEBUG_WRITES=1, else null): the owning warp of output row r
+  // bumps wcount[r] once when it stores the row -- the launcher then checks every count is 1
+  // (reference WriteTracking, tests/test_backward.py:94-108)
+  int32_t* wcount;
 };
+
+MXS_DEV void note_row_write(const GradParams& p, long long r, int lane) {
+  if (p.wcount != nullptr && lane == 0) atomicAdd(p.wcount + r, 1);
+}
 
 // K7: warp per destination row.  Q rows are gathered through L2 (Q is small and hot).
 template <typename T>
@@ -54,6 +62,7 @@ __global__ void __launch_bounds__(256) grad_docs_kernel(const T* __restrict__ Q,
       }
     }
   }
+  note_row_write(p, r, lane);
   float* out = p.dD + r * p.dim;
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
@@ -97,6 +106,7 @@ __global__ void __launch_bounds__(256) grad_query_kernel(const T* __restrict__ D
       }
     }
   }
+  note_row_write(p, wq, lane);
   float* out = p.dQ + wq * p.dim;
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
@@ -204,6 +214,7 @@ __global__ void __launch_bounds__(256) grad_docs_vec_kernel(const T* __restrict_
             for (int v = 0; v < V; ++v) acc[a][v] = __fmaf_rn(w[u], x[u][a][v], acc[a][v]);
     }
   }
+  note_row_write(p, r, lane);
   float* out = p.dD + r * p.dim;
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
@@ -266,6 +277,7 @@ __global__ void __launch_bounds__(256) grad_query_vec_kernel(const T* __restrict
             for (int v = 0; v < V; ++v) acc[a][v] = __fmaf_rn(w[u], x[u][a][v], acc[a][v]);
     }
   }
+  note_row_write(p, wq, lane);
   float* out = p.dQ + wq * p.dim;
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
@@ -391,6 +403,7 @@ __global__ void __launch_bounds__(256) grad_docs_rg_kernel(const T* __restrict__
       grad_rowgroup_accum<T, LPR>(Q, p.dim, rows, ws, acc, lp);
     }
   }
+  note_row_write(p, r, lane);
   grad_rowgroup_store<T, LPR>(acc, p.dD + r * p.dim, lane);
 }
 
@@ -428,7 +441,18 @@ __global__ void __launch_bounds__(256) grad_query_rg_kernel(const T* __restrict_
       grad_rowgroup_accum<T, LPR>(D, p.dim, rows, ws, acc, lp);
     }
   }
+  note_row_write(p, wq, lane);
   grad_rowgroup_store<T, LPR>(acc, p.dQ + wq * p.dim, lane);
+}
+
+// out[0] = number of rows whose write count is not exactly 1, out[1] = the first such row (or -1)
+__global__ void __launch_bounds__(256) write_once_check_kernel(const int32_t* __restrict__ wcount, long long n,
+                                                               unsigned long long* out) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    if (wcount[r] != 1) {
+      atomicAdd(out, 1ull);
+      atomicMin(out + 1, (unsigned long long)r);
+    }
 }
 
 }  // namespace mxs

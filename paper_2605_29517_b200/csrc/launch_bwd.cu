@@ -73,6 +73,40 @@ static bool launch_grad_query_vec(const T* D, const mxs::GradParams& p, long lon
   }
 }
 
+// MXS_DEBUG_WRITES=1: ownership ledger of the destination-owned gathers.  Every output row must
+// be stored by exactly one warp (the reference's WriteTracking assertion, tests/test_backward.py:
+// 94-108); the check is synchronous and reports the first offending row.
+struct WriteLedger {
+  int32_t* counts = nullptr;
+  unsigned long long* result = nullptr;
+  long long n = 0;
+  int arm(mxs::GradParams& p, long long rows, cudaStream_t st) {
+    if (!env_is("MXS_DEBUG_WRITES", "1") || rows < 1) return MXS_OK;
+    n = rows;
+    if (cudaMallocAsync((void**)&counts, (size_t)((rows + 3) & ~3LL) * sizeof(int32_t) + 16, st) != cudaSuccess)
+      return fail(MXS_CUDA_ERROR, "write ledger: allocation failed");
+    result = reinterpret_cast<unsigned long long*>(counts + ((rows + 3) & ~3LL));
+    // counts = 0, result = {0, ~0}: two memsets (0x00 then 0xff over the second word)
+    if (cudaMemsetAsync(counts, 0, (size_t)((rows + 3) & ~3LL) * sizeof(int32_t) + 8, st) != cudaSuccess ||
+        cudaMemsetAsync(result + 1, 0xff, 8, st) != cudaSuccess)
+      return fail(MXS_CUDA_ERROR, "write ledger: memset failed");
+    p.wcount = counts;
+    return MXS_OK;
+  }
+  int check(const char* what, cudaStream_t st) {
+    if (!counts) return MXS_OK;
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 4096);
+    mxs::write_once_check_kernel<<<blocks, 256, 0, st>>>(counts, n, result);
+    unsigned long long h[2] = {0ull, 0ull};
+    cudaMemcpyAsync(h, result, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(counts, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(MXS_CUDA_ERROR, "write ledger: sync failed");
+    if (h[0] != 0)
+      return fail(MXS_CUDA_ERROR, "%s: %llu output rows not written exactly once (first: row %llu)", what, h[0], h[1]);
+    return MXS_OK;
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -181,6 +215,9 @@ int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
   p.n_dest = n_dest;
   p.dD = dD;
   cudaStream_t st = (cudaStream_t)stream;
+  WriteLedger ledger;
+  int s = ledger.arm(p, n_dest, st);
+  if (s != MXS_OK) return s;
   const long long blocks = (n_dest * 32 + 255) / 256;
   if (dtype == MXS_F32) {
     if (!launch_grad_docs_vec<float>((const float*)Q, p, blocks, st))
@@ -193,7 +230,8 @@ int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
       mxs::grad_docs_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)Q, p);
   } else
     return fail(MXS_UNSUPPORTED, "mxs_grad_docs_csr: dtype %d", dtype);
-  return check_launch("grad_docs_kernel");
+  if ((s = check_launch("grad_docs_kernel")) != MXS_OK) return s;
+  return ledger.check("mxs_grad_docs_csr", st);
 }
 
 int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void* D, const int64_t* doc_row_off,
@@ -212,6 +250,9 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
   cudaStream_t st = (cudaStream_t)stream;
   const long long blocks = (n_q * l_q * 32 + 255) / 256;
   if (blocks == 0) return MXS_OK;
+  WriteLedger ledger;
+  int s = ledger.arm(p, n_q * l_q, st);
+  if (s != MXS_OK) return s;
   if (dtype == MXS_F32) {
     if (!launch_grad_query_vec<float>((const float*)D, p, blocks, st))
       mxs::grad_query_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)D, p);
@@ -223,7 +264,8 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
       mxs::grad_query_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>((const __half*)D, p);
   } else
     return fail(MXS_UNSUPPORTED, "mxs_grad_query: dtype %d", dtype);
-  return check_launch("grad_query_kernel");
+  if ((s = check_launch("grad_query_kernel")) != MXS_OK) return s;
+  return ledger.check("mxs_grad_query", st);
 }
 
 }  // extern "C"

@@ -634,3 +634,51 @@ def test_varlen_tensor_core_vs_exact_and_oracle(n_docs, lo, hi, l_q, n_q):
     print(f"varlen: {int((~safe).sum())} of {safe.size} rows excluded (top-2 gap <= {GAP})")
     assert safe.mean() > 0.98
     assert np.array_equal(a_tc.cpu().numpy()[safe], ref_a[safe])
+
+
+@pytest.mark.parametrize("dtype,dim", [(torch.bfloat16, 128), (torch.float32, 40), (torch.float32, 7), (torch.float16, 64)])
+def test_gather_rows_written_exactly_once(monkeypatch, dtype, dim):
+    """Ownership ledger of the destination-owned gathers (MXS_DEBUG_WRITES=1): every dD row and
+    every dQ row is stored by exactly one warp -- the reference's WriteTracking assertion
+    (tests/test_backward.py:94-108) -- on ragged, all-hot and packed maps, through every gather
+    variant (row-group, vectorised, scalar)."""
+    monkeypatch.setenv("MXS_DEBUG_WRITES", "1")
+    rng = np.random.default_rng(dim)
+    Q = torch.from_numpy(rng.standard_normal((3, 70, dim)).astype(np.float32)).cuda().to(dtype)
+    lens = np.array([33, 1, 128, 77], np.int32)
+    D = torch.from_numpy(rng.standard_normal((4, 128, dim)).astype(np.float32)).cuda().to(dtype)
+    g = rng.standard_normal((3, 4))
+    docs = mx.DocBatch.from_dense(D, torch.from_numpy(lens))
+    _, am, _ = mx.fused_score_batch(Q, docs)
+    dq, dd = mx.backward_dispatch(am, g, Q, docs)
+    assert torch.isfinite(dq).all() and torch.isfinite(dd).all()
+    hot = mx.ArgmaxMap(np.zeros((3, 4, 70), np.int32), lens, padded_len=128)  # every source on row 0
+    dq, dd = mx.backward_dispatch(hot, g, Q, docs)
+    assert torch.isfinite(dd).all()
+    packed = mx.ArgmaxMap(am.numpy(), lens, padded_len=None)
+    flat = mx.grad_docs_csr(mx.build_inverse_csr(packed), g, Q)
+    assert flat.shape == (int(lens.sum()), dim)
+
+
+@pytest.mark.parametrize("knob,value", [("MXS_FWD_IMPL", "ss"), ("MXS_RERANK_IMPL", "r3")])
+def test_alternate_forward_kernels_vs_oracle(monkeypatch, knob, value):
+    """The SS-form kernel (fwd_tc: Q streamed through shared memory instead of resident in TMEM)
+    and the three-slot rerank kernel on bf16, forced by their run-time knobs on the ColPali pair
+    shape and a ragged ColBERT shape: scores within 1e-3 of the oracle, clear-gap argmax exact,
+    rerank bits equal to the argmax mode."""
+    monkeypatch.setenv(knob, value)
+    rng = np.random.default_rng(41)
+    for n_q, l_q, n_docs, l_pad in ((1, 1024, 6, 1024), (3, 32, 40, 180)):
+        Q = orc.make_queries(n_q, l_q, 128, seed=int(rng.integers(1 << 30)))
+        lens = rng.integers(1, l_pad + 1, n_docs)
+        lens[0] = l_pad
+        D, vl = orc.padded(orc.make_corpus(n_docs, lens, 128, seed=int(rng.integers(1 << 30))), l_pad)
+        Qr, Dr = cuda(Q, torch.bfloat16), cuda(D, torch.bfloat16)
+        Qo, Do = Qr.float().cpu().numpy(), Dr.float().cpu().numpy()
+        ref_s, ref_a = orc.fused_score_batch(Qo, Do, vl)
+        sc, am, _ = mx.score_dense(Qr, Dr, cuda(vl))
+        assert rel_err(sc.cpu().numpy(), ref_s) < REL
+        safe = top2_gap(Qo, Do, vl) > GAP
+        assert np.array_equal(am.cpu().numpy()[safe], ref_a[safe])
+        s2, _, _ = mx.score_dense(Qr, Dr, cuda(vl), want_argmax=False)
+        assert rel_err(s2.cpu().numpy(), ref_s) < REL
