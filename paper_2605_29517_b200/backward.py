@@ -81,9 +81,13 @@ def csr_tensors(indices: torch.Tensor, dest_off: torch.Tensor, dest_len: torch.T
     col_idx = torch.empty(indices.numel(), dtype=torch.int32, device=dev)
     ws_bytes = int(_lib.load().mxs_csr_workspace_bytes(n_q, n_dest))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    _lib.call("mxs_build_inverse_csr", _dev.ptr(indices.contiguous()), n_q, b, l_q, _dev.ptr(dest_off),
-              _dev.ptr(dest_len), n_dest, max_len, _dev.ptr(row_ptr), _dev.ptr(col_idx), _dev.ptr(ws), ws_bytes,
-              _dev.stream_handle(stream))
+    idx = indices.contiguous()  # bound to a name: alive until the launch is queued
+    with _dev.on_device(idx):
+        _lib.call("mxs_build_inverse_csr", _dev.ptr(idx), n_q, b, l_q, _dev.ptr(dest_off), _dev.ptr(dest_len), n_dest,
+                  max_len, _dev.ptr(row_ptr), _dev.ptr(col_idx), _dev.ptr(ws), ws_bytes,
+                  _dev.stream_handle(stream, dev))
+    for t in (idx, dest_off, dest_len, ws):
+        _dev.keep_alive(t, stream)  # non-current launch stream: the allocator must not recycle them early
     return row_ptr, col_idx, ws_bytes
 
 
@@ -134,8 +138,11 @@ def grad_docs_csr(csr: CsrInverse, upstream, queries, report: TrafficReport | No
         raise StaleCsr("CSR source count disagrees with the argmax shape")
     if out is None:
         out = torch.empty((csr.n_dest, dim), dtype=torch.float32, device=Q.device)
-    _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(csr.row_ptr), _dev.ptr(csr.col_idx), csr.n_dest,
-              _dev.ptr(g), _dev.ptr(Q), n_q, n_docs, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream))
+    with _dev.on_device(Q):
+        _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(csr.row_ptr), _dev.ptr(csr.col_idx), csr.n_dest,
+                  _dev.ptr(g), _dev.ptr(Q), n_q, n_docs, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream, Q.device))
+    for t in (Q, g):
+        _dev.keep_alive(t, stream)
     rep.add_read(csr.n_sources * (4 + dim * Q.element_size()))
     rep.add_write(csr.n_dest * dim * 4)
     return out
@@ -175,8 +182,13 @@ def grad_query(argmax, upstream, docs, stream=None) -> torch.Tensor:
     dim = rows.shape[-1]
     g = _check_upstream(upstream, n_q, b, rows.device)
     out = torch.empty((n_q, l_q, dim), dtype=torch.float32, device=rows.device)
-    _lib.call("mxs_grad_query", _dev.dtype_code(rows), _dev.ptr(am.indices), _dev.ptr(g), _dev.ptr(rows.contiguous()),
-              _dev.ptr(off), n_q, b, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream))
+    rows = rows.contiguous()
+    idx = am.indices.contiguous()
+    with _dev.on_device(rows):
+        _lib.call("mxs_grad_query", _dev.dtype_code(rows), _dev.ptr(idx), _dev.ptr(g), _dev.ptr(rows), _dev.ptr(off),
+                  n_q, b, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream, rows.device))
+    for t in (rows, idx, g, off):
+        _dev.keep_alive(t, stream)
     return out
 
 

@@ -57,22 +57,26 @@ def _as_points(x) -> PointSet:
 
 def _norms(x: torch.Tensor, stream=None) -> torch.Tensor:
     out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
-    _lib.call("mxs_sq_norms", _dev.ptr(x), x.shape[0], x.shape[1], _dev.ptr(out), _dev.stream_handle(stream))
+    with _dev.on_device(x):
+        _lib.call("mxs_sq_norms", _dev.ptr(x), x.shape[0], x.shape[1], _dev.ptr(out), _dev.stream_handle(stream, x.device))
     return out
 
 
 def _nearest(a, an, b, bn, stream=None):
     best = torch.empty(a.shape[0], dtype=torch.float32, device=a.device)
     idx = torch.empty(a.shape[0], dtype=torch.int32, device=a.device)
-    _lib.call("mxs_chamfer_nn", _dev.ptr(a), _dev.ptr(an), a.shape[0], _dev.ptr(b), _dev.ptr(bn), b.shape[0],
-              a.shape[1], _dev.ptr(best), _dev.ptr(idx), _dev.stream_handle(stream))
+    with _dev.on_device(a):
+        _lib.call("mxs_chamfer_nn", _dev.ptr(a), _dev.ptr(an), a.shape[0], _dev.ptr(b), _dev.ptr(bn), b.shape[0],
+                  a.shape[1], _dev.ptr(best), _dev.ptr(idx), _dev.stream_handle(stream, a.device))
     return best, idx
 
 
 def _seq_sum_f64(values: torch.Tensor, stream=None) -> float:
     """Strict left-to-right float64 sum (maxsim/kernels.py:22-26) via the certified rowsum kernel."""
     out = torch.empty(1, dtype=torch.float64, device=values.device)
-    _lib.call("mxs_rowsum", _dev.ptr(values), 1, values.numel(), _dev.ptr(out), _dev.stream_handle(stream))
+    with _dev.on_device(values):
+        _lib.call("mxs_rowsum", _dev.ptr(values), 1, values.numel(), _dev.ptr(out),
+                  _dev.stream_handle(stream, values.device))
     return float(out.item())
 
 
@@ -162,11 +166,12 @@ def chamfer_backward(p_set, s_set, argmin_ps, argmin_sp, upstream: float = 1.0,
     rep.alloc(4 * (rp_s.numel() + ci_s.numel() + rp_p.numel() + ci_p.numel()))
     d_p = torch.empty((p.n, p.dim), dtype=torch.float64, device=p.data.device)
     d_s = torch.empty((s.n, s.dim), dtype=torch.float64, device=p.data.device)
-    st = _dev.stream_handle()
-    _lib.call("mxs_chamfer_grad", _dev.ptr(p.data), p.n, _dev.ptr(s.data), p.dim, _dev.ptr(a1), _dev.ptr(rp_p),
-              _dev.ptr(ci_p), c_ps, c_sp, _dev.ptr(d_p), st)
-    _lib.call("mxs_chamfer_grad", _dev.ptr(s.data), s.n, _dev.ptr(p.data), s.dim, _dev.ptr(a2), _dev.ptr(rp_s),
-              _dev.ptr(ci_s), c_sp, c_ps, _dev.ptr(d_s), st)
+    with _dev.on_device(p.data):
+        st = _dev.stream_handle(None, p.data.device)
+        _lib.call("mxs_chamfer_grad", _dev.ptr(p.data), p.n, _dev.ptr(s.data), p.dim, _dev.ptr(a1), _dev.ptr(rp_p),
+                  _dev.ptr(ci_p), c_ps, c_sp, _dev.ptr(d_p), st)
+        _lib.call("mxs_chamfer_grad", _dev.ptr(s.data), s.n, _dev.ptr(p.data), s.dim, _dev.ptr(a2), _dev.ptr(rp_s),
+                  _dev.ptr(ci_s), c_sp, c_ps, _dev.ptr(d_s), st)
     return d_p, d_s
 
 

@@ -101,8 +101,10 @@ def quantize_tensor(x: torch.Tensor, levels: int = 127, stream=None):
     rows = x.numel() // dim if dim else 0
     q = torch.empty(x.shape, dtype=torch.int8, device=x.device)
     s = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
-    _lib.call("mxs_quantize_per_token", _dev.dtype_code(x), _dev.ptr(x), rows, dim, levels, _dev.ptr(q), _dev.ptr(s),
-              _dev.stream_handle(stream))
+    with _dev.on_device(x):
+        _lib.call("mxs_quantize_per_token", _dev.dtype_code(x), _dev.ptr(x), rows, dim, levels, _dev.ptr(q),
+                  _dev.ptr(s), _dev.stream_handle(stream, x.device))
+    _dev.keep_alive(x, stream)
     return q, s
 
 

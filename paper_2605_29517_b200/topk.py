@@ -65,8 +65,11 @@ def topk(scores: torch.Tensor, k: int, id_offset: int = 0, stream=None):
         return top_s, top_id
     ws_bytes = int(_lib.load().mxs_topk_workspace_bytes(n, k))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=s.device)
-    _lib.call("mxs_topk", _dev.ptr(s), n, k, id_offset, _dev.ptr(top_s), _dev.ptr(top_id), _dev.ptr(ws), ws_bytes,
-              _dev.stream_handle(stream))
+    with _dev.on_device(s):
+        _lib.call("mxs_topk", _dev.ptr(s), n, k, id_offset, _dev.ptr(top_s), _dev.ptr(top_id), _dev.ptr(ws), ws_bytes,
+                  _dev.stream_handle(stream, s.device))
+    for t in (s, ws):
+        _dev.keep_alive(t, stream)
     return top_s, top_id
 
 
@@ -87,8 +90,11 @@ def select_candidates(scores: torch.Tensor, ids: torch.Tensor, k: int, stream=No
     _dev.require_cuda(s, i)
     top_s = torch.empty(k, dtype=torch.float64, device=s.device)
     top_i = torch.empty(k, dtype=torch.int64, device=s.device)
-    _lib.call("mxs_topk_candidates", _dev.ptr(s), _dev.ptr(i), s.numel(), k, _dev.ptr(top_s), _dev.ptr(top_i),
-              _dev.stream_handle(stream))
+    with _dev.on_device(s):
+        _lib.call("mxs_topk_candidates", _dev.ptr(s), _dev.ptr(i), s.numel(), k, _dev.ptr(top_s), _dev.ptr(top_i),
+                  _dev.stream_handle(stream, s.device))
+    for t in (s, i):
+        _dev.keep_alive(t, stream)
     return top_s, top_i
 
 
