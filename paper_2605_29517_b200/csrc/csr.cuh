@@ -23,29 +23,10 @@
 // pairs (cub::DeviceRadixSort, stable by construction) and row_ptr by binary search.
 // Indices are int32 (n_src and n_dest < 2^31 are checked on the host).
 #pragma once
+#include "fastdiv.cuh"
 #include "ptx.cuh"
 
 namespace mxs {
-
-// n / d for 32-bit unsigned n and a run-time invariant d >= 1 (Granlund-Montgomery): a mulhi, a
-// subtract and two shifts instead of the ~20-instruction division subroutine per source.
-struct FastDiv {
-  uint32_t d, m, s1, s2;
-};
-inline FastDiv make_fastdiv(uint32_t d) {
-  uint32_t l = 0;
-  while (l < 32 && (1ull << l) < d) ++l;
-  FastDiv f;
-  f.d = d;
-  f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
-  f.s1 = l < 1 ? l : 1;
-  f.s2 = l > 1 ? l - 1 : 0;
-  return f;
-}
-MXS_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) {
-  const uint32_t t = __umulhi(n, f.m);
-  return (t + ((n - t) >> f.s1)) >> f.s2;
-}
 
 // A lane's walk over the flat sources j = q * L_q + i of one document in steps of 32: the source
 // id (which is also the argmax offset) advances incrementally (no division per step; L_q < 32

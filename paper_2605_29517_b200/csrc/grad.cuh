@@ -7,6 +7,7 @@
 // atomics anywhere.  Lanes split the embedding axis (VEC contiguous elements per lane).
 #pragma once
 #include "convert.cuh"  // to_f32
+#include "fastdiv.cuh"
 
 namespace mxs {
 
@@ -26,6 +27,7 @@ struct GradParams {
   // bumps wcount[r] once when it stores the row -- the launcher then checks every count is 1
   // (reference WriteTracking, tests/test_backward.py:94-108)
   int32_t* wcount;
+  FastDiv per_q_div, lq_div;   // K7 source decoding: s / (n_docs * l_q), rem / l_q
 };
 
 MXS_DEV void note_row_write(const GradParams& p, long long r, int lane) {
@@ -337,19 +339,85 @@ struct Vec16<float> {
   }
 };
 
-constexpr int kGradGU = 4;  // source rows in flight per lane group
+#ifndef MXS_GRAD_GU
+#define MXS_GRAD_GU 8
+#endif
+#ifndef GRAD_LOAD
+#define GRAD_LOAD(p) __ldg(reinterpret_cast<const uint4*>(p))
+#endif
+constexpr int kGradGU = MXS_GRAD_GU;  // source rows per lane group and step
+constexpr int kGradWarps = 8;  // warps per block of the row-group kernels
 
+// Per-warp staging of one chunk of up to 32 sources: (gathered row, weight), written once by the
+// lane that decoded the source and read back as a half-warp broadcast (no per-source shuffles).
+struct GradStage {
+  int row[32];
+  float w[32];
+};
+
+// 16-byte gather load, read-only, not allocated in L1 (the rows are L2-resident and not reused by
+// the SM).
+MXS_DEV uint4 ldg_stream16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <typename T>
+MXS_DEV void unpack16(const uint4& t, float (&o)[Vec16<T>::N]);
+template <>
+MXS_DEV void unpack16<__nv_bfloat16>(const uint4& t, float (&o)[8]) {
+  const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = __uint_as_float(w[i] << 16);
+    o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+MXS_DEV void unpack16<__half>(const uint4& t, float (&o)[8]) {
+  const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+template <>
+MXS_DEV void unpack16<float>(const uint4& t, float (&o)[4]) {
+  o[0] = __uint_as_float(t.x);
+  o[1] = __uint_as_float(t.y);
+  o[2] = __uint_as_float(t.z);
+  o[3] = __uint_as_float(t.w);
+}
+
+// One step = kGradGU source rows per lane group.  Latency is hidden by occupancy (32-40
+// registers, 64 warps per SM), not by deeper per-warp pipelining: a software-pipelined variant
+// (two steps in flight, 70 registers) measured 126 us vs 87 us at C3 (scripts/probe_grad.py).
 template <typename T, int LPR>
-MXS_DEV void grad_rowgroup_accum(const T* __restrict__ base, int dim, const long long (&rows)[kGradGU],
-                                 const float (&ws)[kGradGU], float (&acc)[Vec16<T>::N], int lp) {
-  constexpr int V = Vec16<T>::N;
-  float x[kGradGU][V];
+MXS_DEV void grad_rowgroup_chunk(const T* __restrict__ base, int dim, const GradStage& st, int n,
+                                 float (&acc)[Vec16<T>::N], int h, int lp) {
+  constexpr int V = Vec16<T>::N, SP = 32 / LPR;
+  for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
+    uint4 raw[kGradGU];
+    float ws[kGradGU];
 #pragma unroll
-  for (int u = 0; u < kGradGU; ++u) Vec16<T>::load(base + rows[u] * dim + lp * V, x[u]);
+    for (int u = 0; u < kGradGU; ++u) {
+      const int j = j0 + u * SP + h;  // entries past n hold (row 0, weight 0)
+      ws[u] = st.w[j & 31];
+      raw[u] = GRAD_LOAD(base + (long long)st.row[j & 31] * dim + lp * V);
+    }
 #pragma unroll
-  for (int u = 0; u < kGradGU; ++u)
+    for (int u = 0; u < kGradGU; ++u) {
+      float x[V];
+      unpack16<T>(raw[u], x);
 #pragma unroll
-    for (int v = 0; v < V; v += 2) ffma2_rn(acc[v], acc[v + 1], ws[u], ws[u], x[u][v], x[u][v + 1]);
+      for (int v = 0; v < V; v += 2) ffma2_rn(acc[v], acc[v + 1], ws[u], ws[u], x[v], x[v + 1]);
+    }
+  }
 }
 
 template <typename T, int LPR>
@@ -366,12 +434,16 @@ MXS_DEV void grad_rowgroup_store(float (&acc)[Vec16<T>::N], float* out, int lane
   }
 }
 
-// K7 row-group: warp per destination row (CSR bucket), dim = LPR * V.
+// K7 row-group: warp per destination row (CSR bucket), dim = LPR * V.  Chunks of 32 sources:
+// coalesced col_idx load, source decode (two invariant divisions), weight load, staged in shared
+// memory; then kGradGU rows in flight per lane group.
 template <typename T, int LPR>
-__global__ void __launch_bounds__(256) grad_docs_rg_kernel(const T* __restrict__ Q, const GradParams p) {
-  constexpr int V = Vec16<T>::N, SP = 32 / LPR;
+__global__ void __launch_bounds__(32 * kGradWarps) grad_docs_rg_kernel(const T* __restrict__ Q, const GradParams p) {
+  constexpr int V = Vec16<T>::N;
+  __shared__ GradStage stage[kGradWarps];
   const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, h = lane / LPR, lp = lane % LPR;
+  GradStage& st = stage[threadIdx.x >> 5];
   if (r >= p.n_dest) return;
   float acc[V];
 #pragma unroll
@@ -384,35 +456,29 @@ __global__ void __launch_bounds__(256) grad_docs_rg_kernel(const T* __restrict__
     float my_w = 0.f;
     if (lane < n) {
       const uint32_t s = (uint32_t)__ldg(p.col_idx + t0 + lane);
-      const uint32_t q = s / per_q, rem = s - q * per_q;
-      const uint32_t b = rem / lq, i = rem - b * lq;
+      const uint32_t q = fdiv(s, p.per_q_div), rem = s - q * per_q;
+      const uint32_t b = fdiv(rem, p.lq_div), i = rem - b * lq;
       my_row = (int)(q * lq + i);
       my_w = __ldg(p.g + (long long)q * p.n_docs + b);
     }
-    for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
-      long long rows[kGradGU];
-      float ws[kGradGU];
-#pragma unroll
-      for (int u = 0; u < kGradGU; ++u) {
-        const int j = j0 + u * SP + h;
-        const int rr = __shfl_sync(0xffffffffu, my_row, j & 31);
-        const float ww = __shfl_sync(0xffffffffu, my_w, j & 31);
-        rows[u] = (j < n) ? rr : 0;
-        ws[u] = (j < n) ? ww : 0.f;
-      }
-      grad_rowgroup_accum<T, LPR>(Q, p.dim, rows, ws, acc, lp);
-    }
+    __syncwarp();  // the previous chunk's readers are done with the stage
+    st.row[lane] = my_row;
+    st.w[lane] = my_w;
+    __syncwarp();
+    grad_rowgroup_chunk<T, LPR>(Q, p.dim, st, n, acc, h, lp);
   }
   note_row_write(p, r, lane);
   grad_rowgroup_store<T, LPR>(acc, p.dD + r * p.dim, lane);
 }
 
-// K8 row-group: warp per (q, i) query row, documents b ascending.
+// K8 row-group: warp per (q, i) query row, documents b ascending (chunks of 32 documents).
 template <typename T, int LPR>
-__global__ void __launch_bounds__(256) grad_query_rg_kernel(const T* __restrict__ D, const GradParams p) {
-  constexpr int V = Vec16<T>::N, SP = 32 / LPR;
+__global__ void __launch_bounds__(32 * kGradWarps) grad_query_rg_kernel(const T* __restrict__ D, const GradParams p) {
+  constexpr int V = Vec16<T>::N;
+  __shared__ GradStage stage[kGradWarps];
   const long long wq = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, h = lane / LPR, lp = lane % LPR;
+  GradStage& st = stage[threadIdx.x >> 5];
   if (wq >= (long long)p.n_q * p.l_q) return;
   const int q = (int)(wq / p.l_q), i = (int)(wq % p.l_q);
   float acc[V];
@@ -420,26 +486,18 @@ __global__ void __launch_bounds__(256) grad_query_rg_kernel(const T* __restrict_
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   for (int b0 = 0; b0 < p.n_docs; b0 += 32) {
     const int n = min(32, p.n_docs - b0);
-    long long my_row = 0;
+    int my_row = 0;
     float my_w = 0.f;
     if (lane < n) {
       const int a_ = __ldg(p.argmax + ((long long)q * p.n_docs + b0 + lane) * p.l_q + i);
       my_w = __ldg(p.g + (long long)q * p.n_docs + b0 + lane);
-      my_row = __ldg(p.doc_row_off + b0 + lane) + a_;
+      my_row = (int)(__ldg(p.doc_row_off + b0 + lane) + a_);
     }
-    for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
-      long long rows[kGradGU];
-      float ws[kGradGU];
-#pragma unroll
-      for (int u = 0; u < kGradGU; ++u) {
-        const int j = j0 + u * SP + h;
-        const long long rr = __shfl_sync(0xffffffffu, my_row, j & 31);
-        const float ww = __shfl_sync(0xffffffffu, my_w, j & 31);
-        rows[u] = (j < n) ? rr : 0;
-        ws[u] = (j < n) ? ww : 0.f;
-      }
-      grad_rowgroup_accum<T, LPR>(D, p.dim, rows, ws, acc, lp);
-    }
+    __syncwarp();
+    st.row[lane] = my_row;
+    st.w[lane] = my_w;
+    __syncwarp();
+    grad_rowgroup_chunk<T, LPR>(D, p.dim, st, n, acc, h, lp);
   }
   note_row_write(p, wq, lane);
   grad_rowgroup_store<T, LPR>(acc, p.dQ + wq * p.dim, lane);

@@ -214,6 +214,8 @@ int mxs_grad_docs_csr(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
   p.col_idx = col_idx;
   p.n_dest = n_dest;
   p.dD = dD;
+  p.per_q_div = mxs::make_fastdiv((uint32_t)(n_docs * l_q));
+  p.lq_div = mxs::make_fastdiv((uint32_t)l_q);
   cudaStream_t st = (cudaStream_t)stream;
   WriteLedger ledger;
   int s = ledger.arm(p, n_dest, st);
