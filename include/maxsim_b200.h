@@ -150,6 +150,18 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
                           int32_t* col_idx, void* ws, size_t ws_bytes, void* stream);
 
 /*
+ * FP32 inputs with the reference's exact arithmetic: float64 gradients, accumulated in the
+ * reference's order with rounded f64 products and adds (bit-identical to maxsim/backward.py:135
+ * grad_docs_csr and :218 grad_query).  g is float64 [n_q, n_docs]; dD [n_dest, dim] and
+ * dQ [n_q, l_q, dim] are float64.  Same ownership rules as the entries below.
+ */
+int mxs_grad_docs_csr_f64(const int32_t* row_ptr, const int32_t* col_idx, int64_t n_dest, const double* g,
+                          const float* Q, int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, double* dD,
+                          void* stream);
+int mxs_grad_query_f64(const int32_t* argmax, const double* g, const float* D, const int64_t* doc_row_off, int64_t n_q,
+                       int64_t n_docs, int64_t l_q, int64_t dim, double* dQ, void* stream);
+
+/*
  * Destination-owned document gradient.  Replaces maxsim/backward.py:135 grad_docs_csr.
  *   dD[r] = sum_{s in bucket r} g[q(s), b(s)] * Q[q_row(s)]   (fp32 accumulation, no atomics)
  *   g [n_q, n_docs] f32; Q [n_q, l_q, dim] of `dtype`; dD [n_dest, dim] f32.

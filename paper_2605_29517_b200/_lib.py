@@ -39,6 +39,8 @@ _SIGNATURES = {
     "mxs_build_inverse_csr": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
     "mxs_grad_docs_csr": [c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "mxs_grad_query": [c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "mxs_grad_docs_csr_f64": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
+    "mxs_grad_query_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "mxs_topk_workspace_bytes": [c_i64, c_i64],
     "mxs_topk": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp],
     "mxs_topk_candidates": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],

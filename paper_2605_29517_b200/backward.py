@@ -107,11 +107,11 @@ def build_inverse_csr(argmax, report: TrafficReport | None = None, stream=None) 
                       padded_len=am.padded_len)
 
 
-def _check_upstream(upstream, n_queries: int, n_docs: int, device) -> torch.Tensor:
+def _check_upstream(upstream, n_queries: int, n_docs: int, device, dtype=torch.float32) -> torch.Tensor:
     g = upstream if isinstance(upstream, torch.Tensor) else torch.as_tensor(np.asarray(upstream, dtype=np.float64))
     if tuple(g.shape) != (n_queries, n_docs):
         raise ShapeMismatch(f"upstream gradient shape {tuple(g.shape)}, expected ({n_queries}, {n_docs})")
-    return g.to(device=device, dtype=torch.float32).contiguous()
+    return g.to(device=device, dtype=dtype).contiguous()
 
 
 def _stack_query_rows(queries) -> torch.Tensor:
@@ -126,25 +126,36 @@ def _stack_query_rows(queries) -> torch.Tensor:
 
 def grad_docs_csr(csr: CsrInverse, upstream, queries, report: TrafficReport | None = None, out=None,
                   stream=None) -> torch.Tensor:
-    """Destination-owned document gradient (maxsim/backward.py:135-173) -> flat (n_dest, dim) fp32."""
+    """Destination-owned document gradient (maxsim/backward.py:135-173) -> flat (n_dest, dim).
+
+    FP32 queries: float64, the reference's exact arithmetic and order (bit-identical).  bf16 /
+    fp16 queries (the tensor-core path): fp32 accumulation (north_star: gradients within 1e-3).
+    """
     rep = report if report is not None else TrafficReport()
     Q = _stack_query_rows(queries).contiguous()
     _dev.require_cuda(Q, csr.row_ptr)
     n_q, l_q, dim = Q.shape
     n_docs = csr.src_shape[1]
-    g = _check_upstream(upstream, n_q, n_docs, Q.device)
+    exact = Q.dtype == torch.float32
+    odt = torch.float64 if exact else torch.float32
+    g = _check_upstream(upstream, n_q, n_docs, Q.device, odt)
     csr.check_sources(n_q, n_docs, l_q)
     if csr.n_sources != n_q * n_docs * l_q:
         raise StaleCsr("CSR source count disagrees with the argmax shape")
-    if out is None:
-        out = torch.empty((csr.n_dest, dim), dtype=torch.float32, device=Q.device)
+    if out is None or out.dtype != odt:
+        out = torch.empty((csr.n_dest, dim), dtype=odt, device=Q.device)
     with _dev.on_device(Q):
-        _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(csr.row_ptr), _dev.ptr(csr.col_idx), csr.n_dest,
-                  _dev.ptr(g), _dev.ptr(Q), n_q, n_docs, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream, Q.device))
+        st = _dev.stream_handle(stream, Q.device)
+        if exact:
+            _lib.call("mxs_grad_docs_csr_f64", _dev.ptr(csr.row_ptr), _dev.ptr(csr.col_idx), csr.n_dest, _dev.ptr(g),
+                      _dev.ptr(Q), n_q, n_docs, l_q, dim, _dev.ptr(out), st)
+        else:
+            _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(csr.row_ptr), _dev.ptr(csr.col_idx),
+                      csr.n_dest, _dev.ptr(g), _dev.ptr(Q), n_q, n_docs, l_q, dim, _dev.ptr(out), st)
     for t in (Q, g):
         _dev.keep_alive(t, stream)
     rep.add_read(csr.n_sources * (4 + dim * Q.element_size()))
-    rep.add_write(csr.n_dest * dim * 4)
+    rep.add_write(csr.n_dest * dim * out.element_size())
     return out
 
 
@@ -170,23 +181,35 @@ def _doc_rows(docs):
     if isinstance(docs, torch.Tensor) and docs.dim() == 3:
         b, l, d = docs.shape
         return docs.reshape(b * l, d), torch.arange(b, dtype=torch.int64, device=docs.device) * l
+    if hasattr(docs, "tokens") and hasattr(docs, "cu_seqlens"):  # the reference's PackedCorpus
+        return _doc_rows(PackedCorpus(docs.tokens, docs.cu_seqlens))
+    if hasattr(docs, "valid_lens") and hasattr(docs, "data"):  # the reference's DocBatch
+        return _doc_rows(DocBatch.from_reference(docs))
     raise ShapeMismatch(f"unsupported document container {type(docs).__name__}")
 
 
 def grad_query(argmax, upstream, docs, stream=None) -> torch.Tensor:
-    """Query gradient, a pure gather (maxsim/backward.py:218-231) -> (N_q, L_q, dim) fp32."""
+    """Query gradient, a pure gather (maxsim/backward.py:218-231) -> (N_q, L_q, dim): float64
+    (bit-identical) for fp32 documents, fp32 accumulation for bf16 / fp16."""
     am = as_argmax_map(argmax)
     rows, off = _doc_rows(docs)
     _dev.require_cuda(am.indices, rows)
     n_q, b, l_q = am.indices.shape
     dim = rows.shape[-1]
-    g = _check_upstream(upstream, n_q, b, rows.device)
-    out = torch.empty((n_q, l_q, dim), dtype=torch.float32, device=rows.device)
+    exact = rows.dtype == torch.float32
+    odt = torch.float64 if exact else torch.float32
+    g = _check_upstream(upstream, n_q, b, rows.device, odt)
+    out = torch.empty((n_q, l_q, dim), dtype=odt, device=rows.device)
     rows = rows.contiguous()
     idx = am.indices.contiguous()
     with _dev.on_device(rows):
-        _lib.call("mxs_grad_query", _dev.dtype_code(rows), _dev.ptr(idx), _dev.ptr(g), _dev.ptr(rows), _dev.ptr(off),
-                  n_q, b, l_q, dim, _dev.ptr(out), _dev.stream_handle(stream, rows.device))
+        st = _dev.stream_handle(stream, rows.device)
+        if exact:
+            _lib.call("mxs_grad_query_f64", _dev.ptr(idx), _dev.ptr(g), _dev.ptr(rows), _dev.ptr(off), n_q, b, l_q, dim,
+                      _dev.ptr(out), st)
+        else:
+            _lib.call("mxs_grad_query", _dev.dtype_code(rows), _dev.ptr(idx), _dev.ptr(g), _dev.ptr(rows),
+                      _dev.ptr(off), n_q, b, l_q, dim, _dev.ptr(out), st)
     for t in (rows, idx, g, off):
         _dev.keep_alive(t, stream)
     return out
@@ -211,7 +234,8 @@ def doc_grads_in_layout(flat: torch.Tensor, argmax) -> torch.Tensor:
 
 def backward_dispatch(argmax, upstream, queries, docs, threshold: int = DEFAULT_SCATTER_THRESHOLD,
                       report: TrafficReport | None = None):
-    """Full backward (maxsim/backward.py:258-279) -> (dQ, dD), both fp32.
+    """Full backward (maxsim/backward.py:258-279) -> (dQ, dD): float64 for fp32 inputs (the
+    reference's arithmetic, bit-identical), fp32 accumulation for bf16 / fp16.
 
     The device always runs the atomic-free CSR reduction; `threshold` is accepted for API
     parity (the reference's result contract does not depend on the chosen path).
@@ -221,6 +245,8 @@ def backward_dispatch(argmax, upstream, queries, docs, threshold: int = DEFAULT_
     if not isinstance(docs, DocBatch):
         from .varlen import PackedCorpus
 
+        if hasattr(docs, "tokens") and hasattr(docs, "cu_seqlens") and not isinstance(docs, PackedCorpus):
+            docs = PackedCorpus(docs.tokens, docs.cu_seqlens)  # the reference's PackedCorpus
         if not isinstance(docs, PackedCorpus):
             from .forward import as_docbatch
 

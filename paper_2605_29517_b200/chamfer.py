@@ -17,7 +17,7 @@ from . import _dev, _lib
 from .backward import csr_tensors
 from .errors import DimMismatch, NaNInput, ShapeMismatch, StaleArgmin
 from .instrument import TrafficReport
-from .types import DEFAULT_TILE, TileConfig
+from .types import DEFAULT_TILE, ArgmaxMap, TileConfig
 
 __all__ = ["PointSet", "chamfer_forward", "chamfer_backward", "dense_chamfer_forward", "dense_chamfer_backward"]
 
@@ -149,8 +149,17 @@ def _csr_of(nn: torch.Tensor, n_dest: int):
     return row_ptr, col_idx
 
 
+def _external_csr(builder, nn: torch.Tensor, n_dest: int, dev):
+    """builder(ArgmaxMap of one document of n_dest rows) -> object with row_ptr / col_idx."""
+    am = ArgmaxMap(nn.reshape(1, 1, -1), [n_dest], padded_len=n_dest)
+    csr = builder(am)
+    as_dev = lambda x: torch.as_tensor(np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x)).to(  # noqa: E731
+        device=dev, dtype=torch.int32).contiguous()
+    return as_dev(csr.row_ptr), as_dev(csr.col_idx)
+
+
 def chamfer_backward(p_set, s_set, argmin_ps, argmin_sp, upstream: float = 1.0,
-                     report: TrafficReport | None = None):
+                     report: TrafficReport | None = None, csr_builder=None):
     """Gradient through the fixed nearest-neighbour match (maxsim/chamfer.py:167-218).
 
     Returns (dP, dS) float64 on the device, bit-identical to the reference's loops.
@@ -161,8 +170,12 @@ def chamfer_backward(p_set, s_set, argmin_ps, argmin_sp, upstream: float = 1.0,
     u = float(upstream)
     c_ps = 2.0 * u / p.n
     c_sp = 2.0 * u / s.n
-    rp_s, ci_s = _csr_of(a1, s.n)  # bucket r of S <- sources i of P (dS scatter half)
-    rp_p, ci_p = _csr_of(a2, p.n)  # bucket r of P <- sources j of S (dP scatter half)
+    if csr_builder is None:
+        rp_s, ci_s = _csr_of(a1, s.n)  # bucket r of S <- sources i of P (dS scatter half)
+        rp_p, ci_p = _csr_of(a2, p.n)  # bucket r of P <- sources j of S (dP scatter half)
+    else:  # an external inverse-CSR builder (the drop-in binding's shared-builder hook)
+        rp_s, ci_s = _external_csr(csr_builder, a1, s.n, p.data.device)
+        rp_p, ci_p = _external_csr(csr_builder, a2, p.n, p.data.device)
     rep.alloc(4 * (rp_s.numel() + ci_s.numel() + rp_p.numel() + ci_p.numel()))
     d_p = torch.empty((p.n, p.dim), dtype=torch.float64, device=p.data.device)
     d_s = torch.empty((s.n, s.dim), dtype=torch.float64, device=p.data.device)

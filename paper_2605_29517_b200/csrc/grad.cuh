@@ -503,6 +503,102 @@ __global__ void __launch_bounds__(32 * kGradWarps) grad_query_rg_kernel(const T*
   grad_rowgroup_store<T, LPR>(acc, p.dQ + wq * p.dim, lane);
 }
 
+// ---------------------------------------------------------------------------------------------
+// FP32 inputs, the reference's exact arithmetic: float64 accumulation in the reference's order
+// (maxsim/backward.py:165-172: acc += w[s] * q_row, sources ascending per bucket, a rounded f64
+// product then a rounded f64 add -- no FMA; :225-231: d_q[q] += g[q, b] * D_b[idx], b ascending),
+// so dD and dQ are bit-identical to the reference's float64 gradients.  Warp per output row,
+// lane k owns elements k, k + 32, ... (NC per lane); 32 sources decoded per chunk in parallel.
+struct GradParams64 {
+  int n_q, n_docs, l_q, dim;
+  const double* g;             // [n_q, n_docs]
+  const int32_t* row_ptr;      // K7
+  const int32_t* col_idx;
+  long long n_dest;
+  double* dD;                  // [n_dest, dim]
+  const int32_t* argmax;       // K8
+  const long long* doc_row_off;
+  double* dQ;                  // [n_q, l_q, dim]
+  int32_t* wcount;             // debug ownership ledger (see GradParams)
+};
+
+template <int NC>
+__global__ void __launch_bounds__(256) grad_docs_f64_kernel(const float* __restrict__ Q, const GradParams64 p) {
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= p.n_dest) return;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  const int lo = __ldg(p.row_ptr + r), hi = __ldg(p.row_ptr + r + 1);
+  const long long per_q = (long long)p.n_docs * p.l_q;
+  for (int t0 = lo; t0 < hi; t0 += 32) {
+    const int n = min(32, hi - t0);
+    long long my_row = 0;
+    double my_w = 0.0;
+    if (lane < n) {
+      const long long s = __ldg(p.col_idx + t0 + lane);
+      const long long q = s / per_q, b = (s / p.l_q) % p.n_docs;
+      my_row = q * p.l_q + s % p.l_q;
+      my_w = __ldg(p.g + q * p.n_docs + b);
+    }
+    for (int j = 0; j < n; ++j) {
+      const long long row = __shfl_sync(0xffffffffu, my_row, j);
+      const double w = __shfl_sync(0xffffffffu, my_w, j);
+      const float* src = Q + row * p.dim;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int k = c * 32 + lane;
+        if (k < p.dim) acc[c] = __dadd_rn(acc[c], __dmul_rn(w, (double)__ldg(src + k)));
+      }
+    }
+  }
+  if (p.wcount != nullptr && lane == 0) atomicAdd(p.wcount + r, 1);
+  double* out = p.dD + r * p.dim;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int k = c * 32 + lane;
+    if (k < p.dim) out[k] = acc[c];
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) grad_query_f64_kernel(const float* __restrict__ D, const GradParams64 p) {
+  const long long wq = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wq >= (long long)p.n_q * p.l_q) return;
+  const int q = (int)(wq / p.l_q), i = (int)(wq % p.l_q);
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int b0 = 0; b0 < p.n_docs; b0 += 32) {
+    const int n = min(32, p.n_docs - b0);
+    long long my_row = 0;
+    double my_w = 0.0;
+    if (lane < n) {
+      my_row = __ldg(p.doc_row_off + b0 + lane) + __ldg(p.argmax + ((long long)q * p.n_docs + b0 + lane) * p.l_q + i);
+      my_w = __ldg(p.g + (long long)q * p.n_docs + b0 + lane);
+    }
+    for (int j = 0; j < n; ++j) {
+      const long long row = __shfl_sync(0xffffffffu, my_row, j);
+      const double w = __shfl_sync(0xffffffffu, my_w, j);
+      const float* src = D + row * p.dim;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int k = c * 32 + lane;
+        if (k < p.dim) acc[c] = __dadd_rn(acc[c], __dmul_rn(w, (double)__ldg(src + k)));
+      }
+    }
+  }
+  if (p.wcount != nullptr && lane == 0) atomicAdd(p.wcount + wq, 1);
+  double* out = p.dQ + wq * p.dim;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int k = c * 32 + lane;
+    if (k < p.dim) out[k] = acc[c];
+  }
+}
+
 // out[0] = number of rows whose write count is not exactly 1, out[1] = the first such row (or -1)
 __global__ void __launch_bounds__(256) write_once_check_kernel(const int32_t* __restrict__ wcount, long long n,
                                                                unsigned long long* out) {

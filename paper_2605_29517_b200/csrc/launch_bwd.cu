@@ -80,7 +80,8 @@ struct WriteLedger {
   int32_t* counts = nullptr;
   unsigned long long* result = nullptr;
   long long n = 0;
-  int arm(mxs::GradParams& p, long long rows, cudaStream_t st) {
+  template <typename P>
+  int arm(P& p, long long rows, cudaStream_t st) {
     if (!env_is("MXS_DEBUG_WRITES", "1") || rows < 1) return MXS_OK;
     n = rows;
     if (cudaMallocAsync((void**)&counts, (size_t)((rows + 3) & ~3LL) * sizeof(int32_t) + 16, st) != cudaSuccess)
@@ -106,6 +107,17 @@ struct WriteLedger {
     return MXS_OK;
   }
 };
+
+// f64 gathers for fp32 inputs (bit-identical to the reference's float64 gradients)
+template <typename KernelFn>
+static int launch_f64(KernelFn pick, int64_t dim, long long warps, const char* what, cudaStream_t st) {
+  const long long blocks = (warps * 32 + 255) / 256;
+  if (blocks == 0) return MXS_OK;
+  const int nc = (int)((dim + 31) / 32);
+  if (!pick(nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : nc <= 8 ? 8 : 16, (unsigned)blocks, st))
+    return fail(MXS_UNSUPPORTED, "%s: dim %lld", what, (long long)dim);
+  return check_launch(what);
+}
 
 }  // namespace
 
@@ -268,6 +280,75 @@ int mxs_grad_query(int dtype, const int32_t* argmax, const float* g, const void*
     return fail(MXS_UNSUPPORTED, "mxs_grad_query: dtype %d", dtype);
   if ((s = check_launch("grad_query_kernel")) != MXS_OK) return s;
   return ledger.check("mxs_grad_query", st);
+}
+
+int mxs_grad_docs_csr_f64(const int32_t* row_ptr, const int32_t* col_idx, int64_t n_dest, const double* g,
+                          const float* Q, int64_t n_q, int64_t n_docs, int64_t l_q, int64_t dim, double* dD,
+                          void* stream) {
+  if (!row_ptr || !col_idx || !g || !Q || !dD) return fail(MXS_INVALID_ARGUMENT, "mxs_grad_docs_csr_f64: null pointer");
+  if (dim < 1 || dim > 512) return fail(MXS_UNSUPPORTED, "mxs_grad_docs_csr_f64: dim %lld outside [1, 512]", (long long)dim);
+  if (n_dest < 1) return MXS_OK;
+  mxs::GradParams64 p = {};
+  p.n_q = (int)n_q;
+  p.n_docs = (int)n_docs;
+  p.l_q = (int)l_q;
+  p.dim = (int)dim;
+  p.g = g;
+  p.row_ptr = row_ptr;
+  p.col_idx = col_idx;
+  p.n_dest = n_dest;
+  p.dD = dD;
+  cudaStream_t st = (cudaStream_t)stream;
+  WriteLedger ledger;
+  int s = ledger.arm(p, n_dest, st);
+  if (s != MXS_OK) return s;
+  s = launch_f64(
+      [&](int nc, unsigned blocks, cudaStream_t stm) {
+        switch (nc) {
+          case 1: mxs::grad_docs_f64_kernel<1><<<blocks, 256, 0, stm>>>(Q, p); return true;
+          case 2: mxs::grad_docs_f64_kernel<2><<<blocks, 256, 0, stm>>>(Q, p); return true;
+          case 4: mxs::grad_docs_f64_kernel<4><<<blocks, 256, 0, stm>>>(Q, p); return true;
+          case 8: mxs::grad_docs_f64_kernel<8><<<blocks, 256, 0, stm>>>(Q, p); return true;
+          case 16: mxs::grad_docs_f64_kernel<16><<<blocks, 256, 0, stm>>>(Q, p); return true;
+          default: return false;
+        }
+      },
+      dim, n_dest, "grad_docs_f64_kernel", st);
+  if (s != MXS_OK) return s;
+  return ledger.check("mxs_grad_docs_csr_f64", st);
+}
+
+int mxs_grad_query_f64(const int32_t* argmax, const double* g, const float* D, const int64_t* doc_row_off, int64_t n_q,
+                       int64_t n_docs, int64_t l_q, int64_t dim, double* dQ, void* stream) {
+  if (!argmax || !g || !D || !doc_row_off || !dQ) return fail(MXS_INVALID_ARGUMENT, "mxs_grad_query_f64: null pointer");
+  if (dim < 1 || dim > 512) return fail(MXS_UNSUPPORTED, "mxs_grad_query_f64: dim %lld outside [1, 512]", (long long)dim);
+  mxs::GradParams64 p = {};
+  p.n_q = (int)n_q;
+  p.n_docs = (int)n_docs;
+  p.l_q = (int)l_q;
+  p.dim = (int)dim;
+  p.g = g;
+  p.argmax = argmax;
+  p.doc_row_off = (const long long*)doc_row_off;
+  p.dQ = dQ;
+  cudaStream_t st = (cudaStream_t)stream;
+  WriteLedger ledger;
+  int s = ledger.arm(p, n_q * l_q, st);
+  if (s != MXS_OK) return s;
+  s = launch_f64(
+      [&](int nc, unsigned blocks, cudaStream_t stm) {
+        switch (nc) {
+          case 1: mxs::grad_query_f64_kernel<1><<<blocks, 256, 0, stm>>>(D, p); return true;
+          case 2: mxs::grad_query_f64_kernel<2><<<blocks, 256, 0, stm>>>(D, p); return true;
+          case 4: mxs::grad_query_f64_kernel<4><<<blocks, 256, 0, stm>>>(D, p); return true;
+          case 8: mxs::grad_query_f64_kernel<8><<<blocks, 256, 0, stm>>>(D, p); return true;
+          case 16: mxs::grad_query_f64_kernel<16><<<blocks, 256, 0, stm>>>(D, p); return true;
+          default: return false;
+        }
+      },
+      dim, n_q * l_q, "grad_query_f64_kernel", st);
+  if (s != MXS_OK) return s;
+  return ledger.check("mxs_grad_query_f64", st);
 }
 
 }  // extern "C"

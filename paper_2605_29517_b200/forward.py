@@ -179,8 +179,8 @@ def fused_score_batch(queries, docs, tile: TileConfig = DEFAULT_TILE, report: Tr
     `threads` is accepted for API parity; the device decides its own parallelism.
     Returns (ScoreMatrix, ArgmaxMap, TrafficReport).
     """
-    if not isinstance(tile, TileConfig):
-        raise TypeError("tile must be a TileConfig")
+    if not isinstance(tile, TileConfig) and not all(hasattr(tile, a) for a in ("bq", "bd", "qchunk")):
+        raise TypeError("tile must be a TileConfig")  # ours or the reference's (duck-typed)
     Q = _stack_queries(queries)
     docs = as_docbatch(docs)
     if Q.shape[-1] != docs.dim:
