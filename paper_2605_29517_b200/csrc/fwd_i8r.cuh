@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
               else
                 mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
             }
+            if constexpr (kI8 && MXS_I8_TC_UNBIAS)  // TMEM = f32(acc) exactly (see i2f2_biased)
+              mma_f16_ss(dcol, bias_desc, bias_desc, kBiasIdesc | kIdescNegA, 1u);
             mma_commit(&hdr->tfull[slot]);
           }
           __syncwarp();

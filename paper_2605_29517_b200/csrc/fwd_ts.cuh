@@ -56,8 +56,11 @@ struct TsSmemHeader {
 // K = 16, every 16-byte chunk of which is {2048, 1024, 1024, 0, 0, 0, 0, 0}, so each output is
 // 2 * (2^22 + 2^20 + 2^20) = 1.5 * 2^23 exactly -- the f32 kMagicF whose bits are kMagicI2F --
 // whatever the swizzle.  The kind::i8 MMAs then accumulate (s32, enable_input_d = 1) on top:
-// TMEM = kMagicI2F + acc, |acc| <= 2^21 for d <= 128.  Cost: one K = 16 bf16 MMA per accumulator
-// (+25 % tensor-pipe time on an epilogue-bound kernel).
+// TMEM = kMagicI2F + acc, |acc| <= 2^21 for d <= 128.  A second K = 16 kind::f16 MMA of the same
+// tile with the negate-A bit then adds -kMagicF to the accumulator read as f32 (MXS_I8_TC_UNBIAS,
+// see i2f2_biased), leaving f32(acc) exactly, so the epilogue does no conversion at all.  Cost: two
+// K = 16 bf16 MMAs per accumulator (+50 % tensor-pipe time: measured raw TMA + MMA rate 0.82 ms ->
+// 1.14 ms at C4) on an epilogue-bound kernel (C4 rerank 1.61 -> 1.51 ms).
 constexpr int kBiasTileBytes = 128 * 128;  // one SW128 K-major bf16 atom, 128 rows x 128 B
 MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
   const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
@@ -432,6 +435,8 @@ __global__ void __launch_bounds__(kTsThreads, 1)
               else
                 mma_f16_ts(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
             }
+            if constexpr (kBias && MXS_I8_TC_UNBIAS)  // TMEM = kMagicF + acc - kMagicF (see i2f2_biased)
+              mma_f16_ss(dcol, bias_desc, bias_desc, make_idesc(1, 1, 128, 128) | kIdescNegA, 1u);
             mma_commit(&hdr->tfull[slot]);
           }
           __syncwarp();

@@ -284,8 +284,24 @@ MXS_DEV void i2f2_magic(float& o0, float& o1, uint32_t a0, uint32_t a1) {
 }
 // The same conversion when the s32 accumulator was pre-loaded with the bits of kMagicF (TMEM then
 // holds kMagicI2F + acc, i.e. the f32 value kMagicF + acc): one FADD2, no integer add.
+//
+// With MXS_I8_TC_UNBIAS (default) the tensor core also removes the bias: after the kind::i8 steps
+// one more kind::f16 MMA of the bias tile with the negate-A bit adds -kMagicF to the accumulator
+// read as f32 (kMagicF + acc, exact), so TMEM already holds f32(acc) exactly (an integer of
+// magnitude <= 2^22; every partial of the products and the addend is a multiple of 1 below 2^25)
+// and the epilogue's conversion is free -- the FADD2 moves from the issue-bound epilogue to the
+// tensor pipe, which has slack in this kernel.
+#ifndef MXS_I8_TC_UNBIAS
+#define MXS_I8_TC_UNBIAS 1
+#endif
+constexpr uint32_t kIdescNegA = 1u << 13;  // instruction descriptor: negate A
 MXS_DEV void i2f2_biased(float& o0, float& o1, uint32_t a0, uint32_t a1) {
+#if MXS_I8_TC_UNBIAS
+  o0 = __uint_as_float(a0);
+  o1 = __uint_as_float(a1);
+#else
   fadd2_rn(o0, o1, __uint_as_float(a0), __uint_as_float(a1), -kMagicF, -kMagicF);
+#endif
 }
 // ---------------------------------------------------------------- distributed shared memory
 // Address of the same shared variable in CTA `rank` of the cluster (shared::cluster window).
