@@ -538,7 +538,7 @@ def run_c2(a, rank, world, local_rank, sub):
             "pct_of_tensor_peak": 100.0 * achieved / pk,
             "roofline": {
                 "bound": "tensor",
-                "kernel": "fwd_ts_kernel<BF16,KA=2,CL=2> with the fused f64 score (mxs_fused_score_batch, rowmax = NULL)",
+                "kernel": "fwd_pair_kernel<BF16,KA=2,CL=2,QB=4> (CTA pair, tcgen05 cta_group::2, 3 TMEM accumulator slots) with the fused f64 score (mxs_fused_score_batch, rowmax = NULL)",
                 "achieved": achieved,
                 "peak": pk,
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_src})",

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG_DIR)
 # Translation units (compiled in parallel, then linked); each includes the kernel headers it
 # instantiates, and every kernel header is included by exactly one of them.
 SOURCES = ["host.cu", "capi.cu", "launch_ts_bf16.cu", "launch_ts_f16.cu", "launch_ts_i8.cu", "launch_ss.cu",
-           "launch_r3.cu", "launch_varlen.cu", "launch_exact.cu", "launch_bwd.cu", "launch_misc.cu"]
+           "launch_r3.cu", "launch_pair.cu", "launch_varlen.cu", "launch_exact.cu", "launch_bwd.cu", "launch_misc.cu"]
 OBJ_DIR = os.path.join(LIB_DIR, "obj")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 

@@ -50,7 +50,7 @@ int check_dense_shapes(const char* what, int64_t n_q, int64_t l_q, int64_t n_doc
   return MXS_OK;
 }
 
-// bf16 / fp16 tensor-core dispatch: fwd_i8r (opt-in rerank) -> fwd_ts -> SS fwd_tc -> exact SIMT.
+// bf16 / fp16 tensor-core dispatch: fwd_i8r (opt-in rerank) -> fwd_pair -> fwd_ts -> SS fwd_tc -> exact SIMT.
 // On return *fused says whether `scores` was already written by the kernel's epilogue.
 template <mxs::TcKind KIND>
 int dispatch_float_tc(int dtype, const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad,
@@ -63,6 +63,10 @@ int dispatch_float_tc(int dtype, const void* Q, int64_t n_q, int64_t l_q, const 
               ? MXS_UNSUPPORTED
               : launch_fwd_r3<KIND>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax, scores,
                                     fused, st);
+  // CTA-pair kernel (three accumulator slots) for 256 < L_q <= 1024, d <= 128; MXS_FWD_IMPL=ts
+  // forces the single-CTA kernel
+  if (s == MXS_UNSUPPORTED && use_ts_path() && !env_is("MXS_FWD_IMPL", "ts"))
+    s = launch_fwd_pair<KIND>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, rowmax, argmax, scores, fused, st);
   if (s == MXS_UNSUPPORTED && use_ts_path())
     s = launch_fwd_ts<KIND>(Q, n_q, l_q, D, n_docs, l_pad, dim, valid_lens, nullptr, nullptr, rowmax, argmax, scores,
                             fused, st);

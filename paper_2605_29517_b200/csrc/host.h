@@ -51,6 +51,11 @@ template <mxs::TcKind KIND>
 int launch_fwd_r3(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad, int64_t dim,
                   const int32_t* valid_lens, const float* q_scale, const float* d_scale, float* rowmax,
                   double* scores, int* fused, cudaStream_t st);
+// CTA-pair forward (launch_pair.cu)
+template <mxs::TcKind KIND>
+int launch_fwd_pair(const void* Q, int64_t n_q, int64_t l_q, const void* D, int64_t n_docs, int64_t l_pad,
+                    int64_t dim, const int32_t* valid_lens, float* rowmax, int32_t* argmax, double* scores, int* fused,
+                    cudaStream_t st);
 // varlen rows kernel (launch_varlen.cu)
 template <mxs::TcKind KIND>
 int launch_varlen_tc(const void* Q, int64_t n_q, int64_t l_q, const void* tokens, const int64_t* cu, int64_t n_docs,

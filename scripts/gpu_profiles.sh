@@ -12,8 +12,8 @@ prof() {  # name, kernel regex, skip, env, command...
   ncu -i /tmp/$name.ncu-rep --page details > gpurun_out/ncu_${name}_details.txt 2>/dev/null
   rm -f /tmp/$name.ncu-rep
 }
-prof fwd fwd_ts 3 ARGMAX=0 ncu --set full --clock-control none -k regex:fwd_ts -s 3 -c 1 -o /tmp/fwd -f python scripts/probe_perf.py
-prof fwd_argmax fwd_ts 3 ARGMAX=1 ncu --set full --clock-control none -k regex:fwd_ts -s 3 -c 1 -o /tmp/fwd_argmax -f python scripts/probe_perf.py
+prof fwd fwd_pair 3 ARGMAX=0 ROWMAX=0 ncu --set full --clock-control none -k regex:fwd_pair -s 3 -c 1 -o /tmp/fwd -f python scripts/probe_perf.py
+prof fwd_argmax fwd_pair 3 ARGMAX=1 ROWMAX=0 ncu --set full --clock-control none -k regex:fwd_pair -s 3 -c 1 -o /tmp/fwd_argmax -f python scripts/probe_perf.py
 prof int8 fwd_i8r 2 ARGMAX=0 WHICH=int8 ncu --set full --clock-control none -k regex:fwd_i8r -s 2 -c 1 -o /tmp/int8 -f python scripts/probe_int8_varlen.py
 prof varlen varlen 2 WHICH=varlen ncu --set full --clock-control none -k regex:varlen -s 2 -c 1 -o /tmp/varlen -f python scripts/probe_int8_varlen.py
 prof bwd_dd grad_docs 2 ncu --set full --clock-control none -k regex:grad_docs -s 2 -c 1 -o /tmp/bwd_dd -f python scripts/probe_c3.py

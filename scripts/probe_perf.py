@@ -24,11 +24,12 @@ def P(t):
 
 
 WANT_ARGMAX = os.environ.get("ARGMAX", "1") == "1"
+WANT_ROWMAX = os.environ.get("ROWMAX", "1") == "1"  # 0: fused score only (the bench's rerank call)
 
 
 def go():
     _lib.call("mxs_fused_score_batch", _lib.MXS_BF16, P(Q), 1, lq, P(D), nb, 1024, 128, None, P(scores),
-              P(am) if WANT_ARGMAX else None, P(rm), 0, st)
+              P(am) if WANT_ARGMAX else None, P(rm) if WANT_ROWMAX else None, 0, st)
 
 
 for _ in range(3):

@@ -660,15 +660,17 @@ def test_gather_rows_written_exactly_once(monkeypatch, dtype, dim):
     assert flat.shape == (int(lens.sum()), dim)
 
 
-@pytest.mark.parametrize("knob,value", [("MXS_FWD_IMPL", "ss"), ("MXS_RERANK_IMPL", "r3")])
+@pytest.mark.parametrize("knob,value", [("MXS_FWD_IMPL", "ss"), ("MXS_RERANK_IMPL", "r3"), ("MXS_FWD_IMPL", "ts"),
+                                        ("MXS_FWD_IMPL", "pair")])
 def test_alternate_forward_kernels_vs_oracle(monkeypatch, knob, value):
-    """The SS-form kernel (fwd_tc: Q streamed through shared memory instead of resident in TMEM)
-    and the three-slot rerank kernel on bf16, forced by their run-time knobs on the ColPali pair
-    shape and a ragged ColBERT shape: scores within 1e-3 of the oracle, clear-gap argmax exact,
-    rerank bits equal to the argmax mode."""
+    """The SS-form kernel (fwd_tc: Q streamed through shared memory instead of resident in TMEM),
+    the three-slot rerank kernel, the single-CTA TS kernel (fwd_ts) and the CTA-pair kernel
+    (fwd_pair) on bf16, forced by their run-time knobs on the ColPali pair shape, a 2-pair-cluster
+    ragged shape, a 1-pair shape and a ragged ColBERT shape: scores within 1e-3 of the oracle,
+    clear-gap argmax exact, rerank bits equal to the argmax mode."""
     monkeypatch.setenv(knob, value)
     rng = np.random.default_rng(41)
-    for n_q, l_q, n_docs, l_pad in ((1, 1024, 6, 1024), (3, 32, 40, 180)):
+    for n_q, l_q, n_docs, l_pad in ((1, 1024, 6, 1024), (2, 777, 9, 300), (2, 300, 7, 260), (3, 32, 40, 180)):
         Q = orc.make_queries(n_q, l_q, 128, seed=int(rng.integers(1 << 30)))
         lens = rng.integers(1, l_pad + 1, n_docs)
         lens[0] = l_pad
