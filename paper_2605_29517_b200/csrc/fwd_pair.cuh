@@ -253,7 +253,12 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           for (int mb = 0; mb < QB; ++mb, ++nacc) {
             const uint32_t slot = nacc % kPrSlots, use = nacc / kPrSlots;
             // MXS_DEBUG=3: never wait for the drain (raw MMA + TMA rate; results garbage)
-            if (p.debug != 3) mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
+            if (p.debug != 3) {
+              if (p.mma_spin)
+                mbar_wait(&hdr->tempty[slot], (use & 1u) ^ 1u);
+              else
+                mbar_wait_idle(&hdr->tempty[slot], (use & 1u) ^ 1u);
+            }
             tc_fence_after();
             if (elect_one()) {
               const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);

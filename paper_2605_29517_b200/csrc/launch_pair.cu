@@ -48,6 +48,7 @@ int launch_fwd_pair(const void* Q, int64_t n_q, int64_t l_q, const void* D, int6
   p.scores = fuse ? scores : nullptr;
   p.sum_rows = sum_rows;
   p.debug = dbg;
+  p.mma_spin = env_int("MXS_MMA_SPIN", 0);
   CUtensorMap td;
   const CUtensorMapDataType dt =
       (KIND == mxs::TcKind::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
