@@ -31,10 +31,7 @@ struct RowmaxScratch {
       return MXS_OK;
     }
     st = stream;
-    if (cudaMallocAsync((void**)&ptr, n * sizeof(float), stream) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(MXS_CUDA_ERROR, "row-maxima scratch allocation of %zu bytes failed", n * sizeof(float));
-    }
+    if (int s = scratch_alloc((void**)&ptr, n * sizeof(float), stream)) return s;
     *out = ptr;
     return MXS_OK;
   }

@@ -52,6 +52,34 @@ int sm_count() {
   return n;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default memory pool, whose
+// default release threshold (0) hands memory back to the driver at every synchronisation -- the
+// next allocation then maps fresh pages (~ms).  Keep the pool's memory cached instead (once per
+// device); the scratch it holds is bounded by the largest request (row maxima, CSR temporaries).
+int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st) {
+  const int dev = current_device();
+  static std::mutex mu;
+  static bool done[64] = {false};
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> g(mu);
+    if (!done[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+      done[dev] = true;
+    }
+  }
+  if (cudaMallocAsync(ptr, bytes, st) != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return fail(MXS_CUDA_ERROR, "scratch allocation of %zu bytes failed", bytes);
+  }
+  return MXS_OK;
+}
+
 int ensure_smem(const void* kern, size_t bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> done;

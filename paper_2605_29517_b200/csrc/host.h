@@ -20,6 +20,8 @@ int sm_count();
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per device/context: set it for the current
 // device the first time a kernel needs `bytes` there (cached per (kernel, device)).
 int ensure_smem(const void* kern, size_t bytes);
+// cudaMallocAsync from the device's default pool, kept cached across synchronisations
+int scratch_alloc(void** ptr, size_t bytes, cudaStream_t st);
 int env_int(const char* name, int dflt);
 bool env_is(const char* name, const char* value);
 

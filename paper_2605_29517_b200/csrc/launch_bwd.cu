@@ -84,7 +84,7 @@ struct WriteLedger {
   int arm(P& p, long long rows, cudaStream_t st) {
     if (!env_is("MXS_DEBUG_WRITES", "1") || rows < 1) return MXS_OK;
     n = rows;
-    if (cudaMallocAsync((void**)&counts, (size_t)((rows + 3) & ~3LL) * sizeof(int32_t) + 16, st) != cudaSuccess)
+    if (scratch_alloc((void**)&counts, (size_t)((rows + 3) & ~3LL) * sizeof(int32_t) + 16, st) != MXS_OK)
       return fail(MXS_CUDA_ERROR, "write ledger: allocation failed");
     result = reinterpret_cast<unsigned long long*>(counts + ((rows + 3) & ~3LL));
     // counts = 0, result = {0, ~0}: two memsets (0x00 then 0xff over the second word)
@@ -182,10 +182,8 @@ int mxs_build_inverse_csr(const int32_t* argmax, int64_t n_q, int64_t n_docs, in
     return fail(MXS_CUDA_ERROR, "csr radix sort: temp query failed");
   const size_t arr = ((size_t)n * sizeof(int32_t) + 255) & ~(size_t)255;
   char* buf = nullptr;
-  if (cudaMallocAsync((void**)&buf, 3 * arr + temp, st) != cudaSuccess) {
-    cudaGetLastError();
+  if (scratch_alloc((void**)&buf, 3 * arr + temp, st) != MXS_OK)
     return fail(MXS_CUDA_ERROR, "csr radix sort: cannot allocate %zu bytes of scratch", 3 * arr + temp);
-  }
   int32_t* k0 = (int32_t*)buf;
   int32_t* k1 = (int32_t*)(buf + arr);
   int32_t* v0 = (int32_t*)(buf + 2 * arr);

@@ -211,10 +211,7 @@ __global__ void check_cu_kernel(const long long* __restrict__ cu, long long n_do
 template <typename F>
 int run_check(cudaStream_t st, unsigned long long (&host)[2], F launch) {
   unsigned long long* d = nullptr;
-  if (cudaMallocAsync((void**)&d, 16, st) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(MXS_CUDA_ERROR, "validation scratch allocation failed");
-  }
+  if (scratch_alloc((void**)&d, 16, st) != MXS_OK) return fail(MXS_CUDA_ERROR, "validation scratch allocation failed");
   const unsigned long long init[2] = {~0ull, 0ull};
   cudaMemcpyAsync(d, init, 16, cudaMemcpyHostToDevice, st);
   launch(d);
