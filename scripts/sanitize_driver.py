@@ -1,5 +1,6 @@
 """Small invocations of every device kernel family, for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck): fwd_ts (bf16 with argmax, rerank fused S4), fwd_i8r + fwd_ts INT8,
+synccheck / initcheck): fwd_ts (bf16 with argmax, rerank fused S4), fwd_pair (CTA pairs, QB = 4 / 2),
+fwd_i8r + fwd_ts INT8,
 varlen_rows (bf16, ragged across 128-token tiles), exact fp32, quantiser, CSR (cluster kernel +
 radix-sort path), dD / dQ gathers, top-K, Chamfer.  WHICH=a,b,... selects families."""
 import os
@@ -12,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_29517_b200 as mx  # noqa: E402
 from paper_2605_29517_b200.backward import csr_tensors  # noqa: E402
 
-WHICH = set(os.environ.get("WHICH", "fwd,int8,varlen,exact,quant,csr,grad,topk,chamfer").split(","))
+WHICH = set(os.environ.get("WHICH", "fwd,pair,int8,varlen,exact,quant,csr,grad,topk,chamfer").split(","))
 g = torch.Generator(device="cuda").manual_seed(0)
 
 
@@ -29,6 +30,13 @@ if "fwd" in WHICH:
     s2, _, _ = mx.score_dense(Q, D, vl, want_argmax=False)
     torch.cuda.synchronize()
     print("fwd ok", float(s.sum()), float(s2.sum()))
+if "pair" in WHICH:  # CTA-pair forward: QB = 4 (L_q = 700: TMEM + SS blocks) and QB = 2 (L_q = 384)
+    for lq in (700, 384):
+        Qp = unit(2, lq, 128)
+        sp, ap, _ = mx.score_dense(Qp, D, vl)
+        sp2, _, _ = mx.score_dense(Qp, D, vl, want_argmax=False)
+        torch.cuda.synchronize()
+        print("pair ok", lq, float(sp.sum()), float(sp2.sum()))
 if "int8" in WHICH:
     qq, qs = mx.quant.quantize_tensor(Q.float())
     dq, ds = mx.quant.quantize_tensor(D.float())
