@@ -33,31 +33,41 @@
 
 namespace mxs {
 
-constexpr int kPrSlots = 3;
-constexpr int kPrAccCol0 = 128;  // Q: 2 blocks x KA * 32 columns (<= 128), then 3 x 128 accumulator columns
+#ifndef MXS_PR_WARP_ARRIVE
+#define MXS_PR_WARP_ARRIVE 0  // 1: one fused-score arrive per epilogue warp instead of per lane
+#endif
+constexpr int kPrMaxSlots = 4;
+#ifndef MXS_PR_SCORE_BUFS
+#define MXS_PR_SCORE_BUFS 2
+#endif
+constexpr int kPrScoreBufs = MXS_PR_SCORE_BUFS;  // fused-score row buffers (documents in flight)
+// TMEM: NTS Q blocks x KA * 32 columns (<= 128), then the accumulator slots (4 when no Q block is
+// TMEM-resident, else 3) of 128 columns
+__host__ __device__ constexpr int pr_slots(int nts) { return nts == 0 ? 4 : 3; }
 constexpr int kPrHalfAtom = 64 * 128;  // one 64-row x 128-byte SW128 atom (half a document tile)
 
 struct PrSmemHeader {
   uint64_t full[8];
   uint64_t empty[8];
-  uint64_t tfull[kPrSlots];
-  uint64_t tempty[kPrSlots];
+  uint64_t tfull[kPrMaxSlots];
+  uint64_t tempty[kPrMaxSlots];
   uint64_t qfull;
   uint64_t qsfull;  // QB = 4: the SS Q blocks of both CTAs have landed (leader)
   uint64_t qempty;
-  uint64_t sready[2];
-  uint64_t sfree[2];
-  uint64_t speer[2];
-  uint64_t sdone[2];
+  uint64_t sready[kPrScoreBufs];
+  uint64_t sfree[kPrScoreBufs];
+  uint64_t speer[kPrScoreBufs];
+  uint64_t sdone[kPrScoreBufs];
   uint32_t tmem_base;
   uint32_t pad;
 };
 
 // dynamic smem: SS Q blocks (QB = 4: 2 blocks x KA atoms of 128 rows x 128 B) | document
 // half-tile ring | argmax stash (QB blocks x 128 rows x 32 floats) | fused-score row buffers
-__host__ __device__ inline size_t fwd_pair_smem_bytes(int ka, int qb, int stages, bool stash, int sum_rows) {
-  return 1024 + (size_t)(qb - 2) * ka * kAtomBytes + (size_t)stages * ka * kPrHalfAtom +
-         (stash ? (size_t)qb * 128 * 128 : 0) + (size_t)2 * sum_rows * sizeof(float);
+__host__ __device__ inline size_t fwd_pair_smem_bytes(int ka, int qb, int nts, int stages, bool stash, int sum_rows) {
+  return 1024 + (size_t)(qb - nts) * ka * kAtomBytes + (size_t)stages * ka * kPrHalfAtom +
+         (stash ? (size_t)qb * 128 * 128 : 0) + (size_t)kPrScoreBufs * sum_rows * sizeof(float) +
+         (sum_rows ? (size_t)kPrScoreBufs * 4 * kPartialsPerRank * sizeof(ScorePartial) : 0);
 }
 
 MXS_DEV void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
@@ -103,25 +113,22 @@ MXS_DEV void tma_load_2d_pair(const void* tmap, uint32_t bar_cluster, void* smem
       : "memory");
 }
 
-// Arrive on a (possibly remote) mbarrier with the default release.cta semantics, as CUTLASS's
-// cluster barriers do: enough for TMEM hand-offs, whose ordering comes from the tcgen05 fences,
-// and far cheaper than release.cluster (which compiles to a GPU-scope MEMBAR per arrive).
-MXS_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-
-template <TcKind KIND, int KA, int CL, int QB>
+template <TcKind KIND, int KA, int CL, int QB, int NTS>
 __global__ void __launch_bounds__(kTsThreads, 1)
     fwd_pair_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmQ,
                     const FwdTcParams p) {
   static_assert(KIND != TcKind::I8 && (CL == 2 || CL == 4) && KA >= 1 && KA <= 2, "bf16 / fp16, d <= 128");
   static_assert(QB == 2 || (QB == 4 && CL == 2), "QB = 4 (SS blocks) with single-pair clusters");
+  static_assert(NTS == 2 || (NTS == 0 && QB == 4), "TMEM-resident Q blocks: 2, or 0 (all SS)");
+  constexpr int kSlots = pr_slots(NTS);
+  constexpr int kAccCol0 = NTS * KA * 32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;  // QB = 4: SS Q blocks 2, 3
-  uint8_t* sD = sQ + (size_t)(QB - 2) * KA * kAtomBytes;
+  uint8_t* sD = sQ + (size_t)(QB - NTS) * KA * kAtomBytes;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kPrHalfAtom);
   float* sSum = sBest + (p.argmax ? (size_t)QB * 128 * 32 : 0);
+  ScorePartial* sPart = reinterpret_cast<ScorePartial*>(sSum + (size_t)kPrScoreBufs * p.sum_rows);
   const bool fuse = p.scores != nullptr && p.debug != 3;
   __shared__ PrSmemHeader pr_hdr;
   PrSmemHeader* hdr = &pr_hdr;
@@ -152,17 +159,17 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       mbar_init(&hdr->full[s], 1);   // leader: its producer's expect_tx arrive (+ both CTAs' bytes)
       mbar_init(&hdr->empty[s], 1);  // the leader's multicast commit
     }
-    for (int s = 0; s < kPrSlots; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       mbar_init(&hdr->tfull[s], 1);
       mbar_init(&hdr->tempty[s], 8);  // leader: 4 draining warps of each CTA of the pair
     }
     mbar_init(&hdr->qfull, 2 * kEpiWarps);  // leader: every epilogue warp of the pair
     mbar_init(&hdr->qsfull, 1);             // leader: its TMA warp's expect_tx arrive
     mbar_init(&hdr->qempty, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&hdr->sready[s], 32 * kEpiWarps);
+    for (int s = 0; s < kPrScoreBufs; ++s) {
+      mbar_init(&hdr->sready[s], MXS_PR_WARP_ARRIVE ? kEpiWarps : 32 * kEpiWarps);
       mbar_init(&hdr->sfree[s], 1);
-      mbar_init(&hdr->speer[s], 32 * (CL - 1));
+      mbar_init(&hdr->speer[s], 1);  // rank 0's expect_tx arrive + the other ranks' bulk-copy bytes
       mbar_init(&hdr->sdone[s], 1);
     }
     fence_mbar_init();
@@ -191,14 +198,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
               mbar_wait_idle(&hdr->qempty, qeph);  // every MMA reading the old blocks has completed
               qeph ^= 1;
             }
-            if (half == 0) mbar_arrive_expect_tx(&hdr->qsfull, (uint32_t)(2 * 2 * KA * kAtomBytes));
+            if (half == 0) mbar_arrive_expect_tx(&hdr->qsfull, (uint32_t)(2 * (QB - NTS) * KA * kAtomBytes));
             const uint32_t qbar = mapa_u32(smem_u32(&hdr->qsfull), leader);
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < QB - NTS; ++j)
 #pragma unroll
               for (int a = 0; a < KA; ++a)
                 tma_load_2d_pair(&tmQ, qbar, sQ + (size_t)(j * KA + a) * kAtomBytes, a * 64,
-                                 q * p.l_q + (g * QB + 2 + j) * kTileRows, kEvictLast);
+                                 q * p.l_q + (g * QB + NTS + j) * kTileRows, kEvictLast);
             cur_key = q;
           }
         }
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           const uint64_t bd0 = ddesc0 + (uint64_t)((stage * KA * kPrHalfAtom) >> 4);
 #pragma unroll
           for (int mb = 0; mb < QB; ++mb, ++nacc) {
-            const uint32_t slot = nacc % kPrSlots, use = nacc / kPrSlots;
+            const uint32_t slot = nacc % kSlots, use = nacc / kSlots;
             // MXS_DEBUG=3: never wait for the drain (raw MMA + TMA rate; results garbage)
             if (p.debug != 3) {
               if (p.mma_spin)
@@ -262,14 +269,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             tc_fence_after();
             if (elect_one()) {
               const uint32_t acol = tmem_base + (uint32_t)(mb * kQCols);
-              const uint32_t dcol = tmem_base + (uint32_t)(kPrAccCol0 + slot * 128);
+              const uint32_t dcol = tmem_base + (uint32_t)(kAccCol0 + slot * 128);
 #pragma unroll
               for (int k = 0; k < KA * 4; ++k) {
                 const uint64_t koff = (uint64_t)(((k >> 2) * kPrHalfAtom + (k & 3) * 32) >> 4);
-                if (mb < 2) {
+                if (mb < NTS) {
                   mma_f16_ts_pair(dcol, acol + k * 8, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
                 } else {
-                  const uint64_t qoff = (uint64_t)((((mb - 2) * KA + (k >> 2)) * kAtomBytes + (k & 3) * 32) >> 4);
+                  const uint64_t qoff = (uint64_t)((((mb - NTS) * KA + (k >> 2)) * kAtomBytes + (k & 3) * 32) >> 4);
                   mma_f16_ss_pair(dcol, qdesc0 + qoff, bd0 + koff, kIdesc, k > 0 ? 1u : 0u);
                 }
               }
@@ -293,8 +300,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     }
   } else if (warp == kTsSumWarp) {
     // ------------------------------------------------------------------ fused S4 score
-    if (fuse) fused_score_warp<CL>(p, hdr->sready, hdr->sfree, hdr->speer, hdr->sdone, sSum, u_begin, u_end, decode,
-                                   crank, lane);
+    // profiling knob MXS_DEBUG=6: no score warp and no hand-off (scores invalid)
+    if (fuse && p.debug != 6) fused_score_warp<CL, kPrScoreBufs, true>(p, hdr->sready, hdr->sfree, hdr->speer, hdr->sdone, sSum, u_begin, u_end, decode,
+                                   crank, lane, sPart);
   } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
     // warp w in [2, 10): TMEM lane quadrant w % 4, set j = (w - 2) / 4 owns Q blocks j (TMEM) and
@@ -332,7 +340,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             r[4 * c + 2] = w.z;
             r[4 * c + 3] = w.w;
           }
-          tmem_st32(tmem_base + lane_base + (uint32_t)(wset * kQCols + a * 32), r);
+          if constexpr (NTS > 0) tmem_st32(tmem_base + lane_base + (uint32_t)(wset * kQCols + a * 32), r);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -359,15 +367,16 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         for (int i = 0; i < kNB; ++i) {
           const int mb = wset + 2 * i;
           const uint32_t n = (uint32_t)QB * nt + (uint32_t)mb;
-          const uint32_t slot = n % kPrSlots;
-          mbar_wait(&hdr->tfull[slot], (n / kPrSlots) & 1u);
+          const uint32_t slot = n % kSlots;
+          mbar_wait(&hdr->tfull[slot], (n / kSlots) & 1u);
           tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kPrAccCol0 + slot * 128);
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kAccCol0 + slot * 128);
           const uint32_t tempty_leader = mapa_u32(smem_u32(&hdr->tempty[slot]), leader);
-          if (p.debug == 2) {  // profiling knob: release the slot unread
+          if (p.debug == 2) {  // profiling knob: release the slot unread (finite maxima for the fused sum)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader);
+            m[i] = 0.f;
             continue;
           }
           float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * 32 : nullptr;
@@ -401,14 +410,26 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         }
       }
       if (fuse) {  // row maxima -> this CTA's row buffer, then every lane arrives (CTA scope)
-        const uint32_t sb = ndoc & 1u;
-        mbar_wait(&hdr->sfree[sb], ((ndoc >> 1) & 1u) ^ 1u);
+        const uint32_t sb = ndoc % kPrScoreBufs;
+        // profiling knob MXS_DEBUG=6: no hand-off at all (scores invalid)
+        if (p.debug != 6) mbar_wait(&hdr->sfree[sb], ((ndoc / kPrScoreBufs) & 1u) ^ 1u);
+        bool valid[kNB];
 #pragma unroll
         for (int i = 0; i < kNB; ++i) {
           const int row = (g * QB + wset + 2 * i) * kTileRows + row_local;
-          if (row < p.l_q) sSum[sb * p.sum_rows + row] = m[i];
+          valid[i] = row < p.l_q;
+          if (valid[i]) sSum[sb * p.sum_rows + row] = m[i];
         }
-        mbar_arrive(&hdr->sready[sb]);
+        // this warp's certified partial sum (the score warp only combines the 8 x CL partials)
+        store_score_partial<kNB>(m, valid, sPart + (sb * CL + crank) * kPartialsPerRank + ((int)warp - kTsEpiWarp0),
+                                 lane);
+        fence_proxy_async();  // the row maxima are shipped to cluster rank 0 by a bulk (async-proxy) copy
+#if MXS_PR_WARP_ARRIVE
+        __syncwarp();  // orders every lane's row store before lane 0's release-arrive
+        if (lane == 0) mbar_arrive(&hdr->sready[sb]);
+#else
+        if (p.debug != 6) mbar_arrive(&hdr->sready[sb]);
+#endif
         ++ndoc;
       }
 #pragma unroll

@@ -218,40 +218,130 @@ MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m
   }
 }
 
-// Score warp of the fused S4 epilogue (fwd_ts_kernel, fwd_i8r_kernel).  The CTA's producers store
-// the row maxima of document n into row buffer [n & 1] of their OWN shared memory and arrive on
-// sready[n & 1] (CTA scope) -- nothing cluster-wide on the epilogue's critical path.  The score
-// warp of rank r != 0 copies its rows into rank 0's buffer through DSMEM (once rank 0 has
-// consumed that buffer's previous document: sdone) and arrives on rank 0's speer (release,
-// cluster scope); the score warp of rank 0 then holds all L_q maxima locally, computes the
-// certified f64 sum and writes the score.  sfree[n & 1] re-arms a CTA's own buffer.
-template <int CL, typename Decode>
+// Score warp of the fused S4 epilogue (fwd_ts_kernel, fwd_pair_kernel).  The CTA's producers store
+// the row maxima of document n into row buffer [n & 1] of their OWN shared memory, fence them to
+// the async proxy and arrive on sready[n & 1] (CTA scope) -- nothing cluster-wide on the
+// epilogue's critical path.  The score warp of rank r != 0 ships its rows into rank 0's buffer
+// with ONE bulk copy (cp.async.bulk shared::cta -> shared::cluster, completing as transaction
+// bytes on rank 0's speer) once rank 0 has consumed that buffer's previous document (sdone); rank
+// 0's score warp arms speer with the other ranks' bytes, then holds all L_q maxima locally,
+// computes the certified f64 sum and writes the score.  sfree[n & 1] re-arms a CTA's own buffer.
+// (Round 2 first pushed the rows with per-lane st.shared::cluster stores and release.cluster
+// arrives: their GPU-scope fences stalled the SM's tensor pipeline, 9 % of the C2 forward.)
+MXS_DEV void bulk_copy_to_cluster(uint32_t dst_cluster, const void* src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+MXS_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// Rows [r0, r1) of rank r's share of a fused-score row buffer, padded to whole 16-byte chunks
+// (the buffers hold whole 128-row blocks, so the padding stays inside them).
+MXS_DEV uint32_t score_rows_bytes(int r0, int r1) { return (uint32_t)(((r1 - r0) + 3) & ~3) * 4u; }
+#ifndef MXS_SCORE_WAIT_SPIN
+#define MXS_SCORE_WAIT_SPIN 0  // 1: the score warps spin on their barriers instead of suspending
+#endif
+MXS_DEV void score_wait(uint64_t* bar, uint32_t parity) {
+#if MXS_SCORE_WAIT_SPIN
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_idle(bar, parity);
+#endif
+}
+MXS_DEV void score_wait_cluster(uint64_t* bar, uint32_t parity) {
+#if MXS_SCORE_WAIT_SPIN
+  mbar_wait_cluster(bar, parity);
+#else
+  mbar_wait_cluster_idle(bar, parity);
+#endif
+}
+// Certified partial sum of one epilogue warp's row maxima (PART mode of fused_score_warp): 16 bytes.
+struct ScorePartial {
+  double s;
+  uint32_t e;  // emin | emax << 8 | finite << 16
+  uint32_t pad;
+};
+constexpr int kPartialsPerRank = 8;  // one per epilogue warp
+// Every lane of an epilogue warp: fold its row maxima v[0..k) (rows >= L_q excluded by the caller)
+// into the warp's certified partial sum; lane 0 stores it.
+template <int K>
+MXS_DEV void store_score_partial(const float (&v)[K], const bool (&valid)[K], ScorePartial* dst, uint32_t lane) {
+  CertSum c;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (valid[i]) c.add(v[i]);
+  c.warp_reduce();
+  if (lane == 0) *dst = ScorePartial{c.s, (uint32_t)c.emin | ((uint32_t)c.emax << 8) | ((c.finite ? 1u : 0u) << 16), 0u};
+}
+
+// PART = false: the score warp folds the L_q row maxima itself; PART = true: every epilogue warp
+// has already folded its rows into a certified partial (store_score_partial, spread over the four
+// SM sub-partitions) and the score warp only combines CL x 8 partials -- the same certificate
+// covers every subset sum, so the result is the same exact sum; the raw rows still travel for the
+// rare sequential fallback.
+template <int CL, int NB = 2, bool PART = false, typename Decode>
 MXS_DEV void fused_score_warp(const FwdTcParams& p, uint64_t* sready, uint64_t* sfree, uint64_t* speer,
                               uint64_t* sdone, float* sSum, long long u_begin, long long u_end, Decode decode,
-                              int crank, uint32_t lane) {
+                              int crank, uint32_t lane, ScorePartial* sPart = nullptr) {
+  const int rows_per_rank = p.qb * kTileRows;
+  uint32_t peer_bytes = 0;  // rank 0: bytes the other ranks ship per document
+  for (int r = 1; r < CL; ++r) {
+    const int r0 = r * rows_per_rank, r1 = min(p.l_q, r0 + rows_per_rank);
+    if (r1 > r0) peer_bytes += score_rows_bytes(r0, r1) + (PART ? kPartialsPerRank * sizeof(ScorePartial) : 0);
+  }
   uint32_t n = 0;
   for (long long u = u_begin; u < u_end; ++u, ++n) {
-    const uint32_t sb = n & 1u, ph = (n >> 1) & 1u;
+    const uint32_t sb = n % NB, ph = (n / NB) & 1u;  // NB row buffers in flight
     float* buf = sSum + sb * p.sum_rows;
-    mbar_wait_idle(&sready[sb], ph);  // this CTA's rows are in
+    score_wait(&sready[sb], ph);  // this CTA's rows are in
     if (crank == 0) {
       int q, g, b;
       decode(u, q, g, b);
-      if constexpr (CL > 1) mbar_wait_cluster_idle(&speer[sb], ph);  // and every other rank's
-      const double sc = warp_score_sum(buf, p.l_q);
+      if constexpr (CL > 1) {
+        if (lane == 0) mbar_arrive_expect_tx(&speer[sb], peer_bytes);
+        score_wait(&speer[sb], ph);  // and every other rank's (bulk copies landed)
+      }
+      double sc;
+      if constexpr (PART) {
+        const ScorePartial* part = sPart + sb * CL * kPartialsPerRank;
+        CertSum c;
+        if (lane < (uint32_t)(CL * kPartialsPerRank)) {
+          const ScorePartial e = part[lane];
+          c.s = e.s;
+          c.emin = (int)(e.e & 0xffu);
+          c.emax = (int)((e.e >> 8) & 0xffu);
+          c.finite = (e.e >> 16) & 1u;
+        }
+        c.warp_reduce();
+        sc = c.exact(p.l_q) ? c.s : warp_score_sum(buf, p.l_q);  // the latter: the sequential chain
+      } else {
+        sc = p.debug == 7 ? 0.0 : warp_score_sum(buf, p.l_q);  // 7: profiling, no sum
+      }
       if (lane == 0) p.scores[(long long)q * p.n_docs + b] = sc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&sfree[sb]);
-      if constexpr (CL > 1) {  // release: rank `lane` may refill our buffer [sb]
-        if (lane >= 1 && lane < (uint32_t)CL) mbar_arrive_cluster(mapa_u32(smem_u32(&sdone[sb]), lane));
+      if constexpr (CL > 1) {  // rank `lane` may refill our buffer [sb] (our reads are done: sc depends on them)
+        if (lane >= 1 && lane < (uint32_t)CL) mbar_arrive_remote(mapa_u32(smem_u32(&sdone[sb]), lane));
       }
     } else if constexpr (CL > 1) {
-      mbar_wait_cluster_idle(&sdone[sb], ph ^ 1u);  // rank 0 consumed its buffer [sb] two documents ago
-      const int r0 = crank * p.qb * kTileRows, r1 = min(p.l_q, r0 + p.qb * kTileRows);
-      for (int i = r0 + (int)lane; i < r1; i += 32) st_cluster_f32(mapa_u32(smem_u32(buf + i), 0u), buf[i]);
-      mbar_arrive_cluster(mapa_u32(smem_u32(&speer[sb]), 0u));  // every lane: release of its own stores
+      const int r0 = crank * rows_per_rank, r1 = min(p.l_q, r0 + rows_per_rank);
+      if (lane == 0) {
+        score_wait_cluster(&sdone[sb], ph ^ 1u);  // rank 0 consumed its buffer [sb] NB documents ago
+        if (r1 > r0) {
+          bulk_copy_to_cluster(mapa_u32(smem_u32(buf + r0), 0u), buf + r0, score_rows_bytes(r0, r1),
+                               mapa_u32(smem_u32(&speer[sb]), 0u));
+          if constexpr (PART) {
+            ScorePartial* part = sPart + sb * CL * kPartialsPerRank + crank * kPartialsPerRank;
+            bulk_copy_to_cluster(mapa_u32(smem_u32(part), 0u), part, kPartialsPerRank * sizeof(ScorePartial),
+                                 mapa_u32(smem_u32(&speer[sb]), 0u));
+          }
+          bulk_wait_read_all();  // our buffer has been read: it may be refilled
+        }
+        mbar_arrive(&sfree[sb]);
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sfree[sb]);
     }
   }
 }
@@ -319,7 +409,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&hdr->sready[s], 32 * kEpiWarps);  // every epilogue lane of this CTA
       mbar_init(&hdr->sfree[s], 1);
-      mbar_init(&hdr->speer[s], CL > 1 ? 32 * (CL - 1) : 1);
+      mbar_init(&hdr->speer[s], 1);  // rank 0's expect_tx arrive + the other ranks' bulk-copy bytes
       mbar_init(&hdr->sdone[s], 1);
     }
     fence_mbar_init();
@@ -650,6 +740,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           const int row = (g * p.qb + mb) * kTileRows + row_local;
           if (mb < qbv && row < p.l_q) dst[row] = m[i];
         }
+        fence_proxy_async();  // the row maxima are shipped to cluster rank 0 by a bulk (async-proxy) copy
         mbar_arrive(&hdr->sready[sb]);
         ++ndoc;
       }

@@ -21,12 +21,15 @@ int launch_fwd_pair(const void* Q, int64_t n_q, int64_t l_q, const void* D, int6
   // MXS_PAIR_CL=4 selects two pairs of TMEM-only CTAs for L_q > 512 (4-CTA clusters: 132 SMs)
   const int cl = (nmb > 4 && env_int("MXS_PAIR_CL", 2) == 4) ? 4 : 2;
   const int qb = nmb <= 4 || cl == 4 ? 2 : 4;
+  // QB = 4 rerank: all four Q blocks in shared memory (SS) leaves TMEM to FOUR accumulator slots
+  // (MXS_PAIR_SS=1); the argmax stash does not fit next to them
+  const int nts = (qb == 4 && argmax == nullptr && env_int("MXS_PAIR_SS", 0) == 1) ? 0 : 2;
   const int dbg = env_int("MXS_DEBUG", 0);
   const bool fuse = scores != nullptr && dbg != 3 && env_int("MXS_FWD_FUSE", 1) != 0;
   if (!fuse && !rowmax) return MXS_UNSUPPORTED;
   const int sum_rows = fuse ? cl * qb * 128 : 0;
   const size_t max_smem = 232448 - sizeof(mxs::PrSmemHeader);
-  const size_t fixed = mxs::fwd_pair_smem_bytes(ka, qb, 0, argmax != nullptr, sum_rows);
+  const size_t fixed = mxs::fwd_pair_smem_bytes(ka, qb, nts, 0, argmax != nullptr, sum_rows);
   int stages = (int)((max_smem - fixed) / ((size_t)ka * mxs::kPrHalfAtom));
   if (stages > 8) stages = 8;
   if (stages < 2) return MXS_UNSUPPORTED;
@@ -56,20 +59,22 @@ int launch_fwd_pair(const void* Q, int64_t n_q, int64_t l_q, const void* D, int6
   CUtensorMap tq;
   if ((s = make_tmap_2d(&td, D, dt, 2, dim, n_docs * l_pad, 64)) != MXS_OK) return s;
   if ((s = make_tmap_2d(&tq, Q, dt, 2, dim, n_q * l_q, 128)) != MXS_OK) return s;
-  const size_t smem = mxs::fwd_pair_smem_bytes(ka, qb, stages, argmax != nullptr, sum_rows);
+  const size_t smem = mxs::fwd_pair_smem_bytes(ka, qb, nts, stages, argmax != nullptr, sum_rows);
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const mxs::FwdTcParams);
   KernT kern = nullptr;
-  if (qb == 4)
-    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 2, 4> : mxs::fwd_pair_kernel<KIND, 2, 2, 4>;
+  if (qb == 4 && nts == 0)
+    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 2, 4, 0> : mxs::fwd_pair_kernel<KIND, 2, 2, 4, 0>;
+  else if (qb == 4)
+    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 2, 4, 2> : mxs::fwd_pair_kernel<KIND, 2, 2, 4, 2>;
   else if (cl == 2)
-    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 2, 2> : mxs::fwd_pair_kernel<KIND, 2, 2, 2>;
+    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 2, 2, 2> : mxs::fwd_pair_kernel<KIND, 2, 2, 2, 2>;
   else
-    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 4, 2> : mxs::fwd_pair_kernel<KIND, 2, 4, 2>;
+    kern = ka == 1 ? mxs::fwd_pair_kernel<KIND, 1, 4, 2, 2> : mxs::fwd_pair_kernel<KIND, 2, 4, 2, 2>;
   if ((s = ensure_smem((const void*)kern, smem)) != MXS_OK) return s;
   const int nsm = sm_count();
   if (nsm <= 0) return fail(MXS_CUDA_ERROR, "no CUDA device");
   long long workers = resident_clusters((const void*)kern, cl, mxs::kTsThreads, smem, nsm);
-  if (env_int("MXS_PRINT_GRID", 0)) fprintf(stderr, "fwd_pair: cl=%d qb=%d clusters=%lld stages=%d\n", cl, qb, workers, stages);
+  if (env_int("MXS_PRINT_GRID", 0)) fprintf(stderr, "fwd_pair: cl=%d qb=%d nts=%d clusters=%lld stages=%d\n", cl, qb, nts, workers, stages);
   if (p.n_units < workers) workers = p.n_units;
   if (workers <= 0) return MXS_OK;
   void* args[] = {(void*)&td, (void*)&tq, (void*)&p};

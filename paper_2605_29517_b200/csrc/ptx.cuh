@@ -322,6 +322,12 @@ MXS_DEV void st_cluster_f32(uint32_t cluster_addr, float v) {
 MXS_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive on a (possibly remote) mbarrier with the default release.cta semantics, as CUTLASS's
+// cluster barriers do: enough for hand-offs whose data moves through the tensor core / TMEM or the
+// async proxy, and far cheaper than release.cluster (which compiles to a GPU-scope MEMBAR).
+MXS_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // Wait on a local mbarrier whose arrivals come from other CTAs (acquire at cluster scope).
 MXS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

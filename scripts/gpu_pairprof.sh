@@ -1,7 +1,6 @@
-# ncu of the CTA-pair forward (rerank, C2 shape) + its cluster count
+# ncu of the CTA-pair forward (rerank, C2 shape): full kernel vs raw pipeline (MXS_DEBUG=3)
 mkdir -p gpurun_out
-MXS_PRINT_GRID=1 MXS_FWD_IMPL=pair ARGMAX=0 NB=2000 REPS=2 python scripts/probe_perf.py 2>&1 | tail -3
-MXS_FWD_IMPL=pair ARGMAX=0 NB=2000 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_pair -s 2 -c 1 -o gpurun_out/pair -f python scripts/probe_perf.py > gpurun_out/ncu_pair.log 2>&1
-python scripts/ncu_hotlines.py gpurun_out/pair.ncu-rep 40 > gpurun_out/pair_hot.txt 2>&1
-python scripts/ncu_summary.py gpurun_out/pair.ncu-rep gpurun_out/ncu_pair.json "pair fwd" > /dev/null 2>&1
-ncu -i gpurun_out/pair.ncu-rep --page details > gpurun_out/ncu_pair_details.txt 2>/dev/null
+for d in 0 2 3; do
+MXS_DEBUG=$d ARGMAX=0 ROWMAX=0 NB=2000 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_pair -s 2 -c 1 -o gpurun_out/pair_d$d -f python scripts/probe_perf.py > gpurun_out/ncu_pair_d$d.log 2>&1
+python scripts/ncu_summary.py gpurun_out/pair_d$d.ncu-rep gpurun_out/ncu_pair_d$d.json "pair fwd debug=$d" > /dev/null 2>&1
+done

@@ -18,5 +18,5 @@ prof int8 fwd_i8r 2 ARGMAX=0 WHICH=int8 ncu --set full --clock-control none -k r
 prof varlen varlen 2 WHICH=varlen ncu --set full --clock-control none -k regex:varlen -s 2 -c 1 -o /tmp/varlen -f python scripts/probe_int8_varlen.py
 prof bwd_dd grad_docs 2 ncu --set full --clock-control none -k regex:grad_docs -s 2 -c 1 -o /tmp/bwd_dd -f python scripts/probe_c3.py
 prof bwd_dq grad_query 2 ncu --set full --clock-control none -k regex:grad_query -s 2 -c 1 -o /tmp/bwd_dq -f python scripts/probe_c3.py
-prof csr csr_place 2 ncu --set full --clock-control none -k regex:csr_place -s 2 -c 1 -o /tmp/csr -f python scripts/probe_c3.py
+prof csr csr_doc 2 ncu --set full --clock-control none -k regex:csr_doc -s 2 -c 1 -o /tmp/csr -f python scripts/probe_c3.py
 ls -la gpurun_out
