@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   } else if (warp == kTsSumWarp) {
     // ------------------------------------------------------------------ fused S4 score
     // profiling knob MXS_DEBUG=6: no score warp and no hand-off (scores invalid)
-    if (fuse && p.debug != 6) fused_score_warp<CL, kPrScoreBufs, true>(p, hdr->sready, hdr->sfree, hdr->speer, hdr->sdone, sSum, u_begin, u_end, decode,
+    if (fuse && p.debug != 6 && p.debug < 8) fused_score_warp<CL, kPrScoreBufs, true>(p, hdr->sready, hdr->sfree, hdr->speer, hdr->sdone, sSum, u_begin, u_end, decode,
                                    crank, lane, sPart);
   } else {
     // ------------------------------------------------------------------ epilogue (+ Q -> TMEM)
@@ -317,6 +317,34 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const uint32_t qfull_leader = mapa_u32(smem_u32(&hdr->qfull), leader);
     uint32_t qeph = 0, ndoc = 0, nt = 0;  // nt: tiles drained so far (accumulator n = QB nt + mb)
     long long cur_key = -1;
+    // At the end of a document each warp folds its rows into an integer fixed-point partial
+    // (store_score_partial; deferring it past the next document's first slot release measured the
+    // same) and arrives; the score warp combines the partials.
+    int pend_sb = -1;  // row buffer of the document whose partial is pending, -1: none
+    auto flush_partial = [&]() {
+      if (pend_sb >= 0) {
+        if (p.debug != 8 && p.debug != 9) {  // profiling knobs (scores invalid): 8 = no partial, no fence; 9 = no partial
+          float pm[kNB];  // this thread's row maxima, back from the row buffer (no registers held across the drain)
+          bool pv[kNB];
+#pragma unroll
+          for (int i = 0; i < kNB; ++i) {
+            const int row = (crank * QB + wset + 2 * i) * kTileRows + row_local;
+            pv[i] = row < p.l_q;
+            pm[i] = pv[i] ? sSum[pend_sb * p.sum_rows + row] : 0.f;
+          }
+          store_score_partial<kNB>(pm, pv, sPart + (pend_sb * CL + crank) * kPartialsPerRank + ((int)warp - kTsEpiWarp0),
+                                   lane, p.l_q);
+        }
+        if (p.debug != 8) fence_proxy_async();  // rows + partial travel to cluster rank 0 by bulk (async-proxy) copy
+#if MXS_PR_WARP_ARRIVE
+        __syncwarp();  // orders every lane's stores before lane 0's release-arrive
+        if (lane == 0) mbar_arrive(&hdr->sready[pend_sb]);
+#else
+        if (p.debug != 6 && p.debug < 8) mbar_arrive(&hdr->sready[pend_sb]);
+#endif
+        pend_sb = -1;
+      }
+    };
     for (long long u = u_begin; u < u_end; ++u) {
       int q, g, b;
       decode(u, q, g, b);
@@ -412,24 +440,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       if (fuse) {  // row maxima -> this CTA's row buffer, then every lane arrives (CTA scope)
         const uint32_t sb = ndoc % kPrScoreBufs;
         // profiling knob MXS_DEBUG=6: no hand-off at all (scores invalid)
-        if (p.debug != 6) mbar_wait(&hdr->sfree[sb], ((ndoc / kPrScoreBufs) & 1u) ^ 1u);
-        bool valid[kNB];
+        if (p.debug != 6 && p.debug < 8) mbar_wait(&hdr->sfree[sb], ((ndoc / kPrScoreBufs) & 1u) ^ 1u);
 #pragma unroll
         for (int i = 0; i < kNB; ++i) {
           const int row = (g * QB + wset + 2 * i) * kTileRows + row_local;
-          valid[i] = row < p.l_q;
-          if (valid[i]) sSum[sb * p.sum_rows + row] = m[i];
+          if (row < p.l_q) sSum[sb * p.sum_rows + row] = m[i];
         }
-        // this warp's certified partial sum (the score warp only combines the 8 x CL partials)
-        store_score_partial<kNB>(m, valid, sPart + (sb * CL + crank) * kPartialsPerRank + ((int)warp - kTsEpiWarp0),
-                                 lane);
-        fence_proxy_async();  // the row maxima are shipped to cluster rank 0 by a bulk (async-proxy) copy
-#if MXS_PR_WARP_ARRIVE
-        __syncwarp();  // orders every lane's row store before lane 0's release-arrive
-        if (lane == 0) mbar_arrive(&hdr->sready[sb]);
-#else
-        if (p.debug != 6) mbar_arrive(&hdr->sready[sb]);
-#endif
+        pend_sb = (int)sb;
+        flush_partial();  // this warp's fixed-point partial, then the rows + partial are ready for the score warp
         ++ndoc;
       }
 #pragma unroll

@@ -258,22 +258,82 @@ MXS_DEV void score_wait_cluster(uint64_t* bar, uint32_t parity) {
 #endif
 }
 // Certified partial sum of one epilogue warp's row maxima (PART mode of fused_score_warp): 16 bytes.
+// Certified partial of one epilogue warp's row maxima (PART mode of fused_score_warp), 16 bytes, in
+// INTEGER fixed point: k = sum of the values in units of 2^(emax - 150 - S) (emax = the warp's
+// largest biased exponent, S = 29 - ceil(log2 L_q)), plus the exponent range and finiteness for the
+// certificate (score_sum.cuh).  Under the certificate (emax - emin <= S over the whole document)
+// every value is an exact integer multiple of that unit, every partial and the total are exact
+// int64 sums, and re-basing a partial to the document's emax is an exact right shift (its lowest
+// set bit sits at >= emin - emax_doc + S >= 0) -- so the result is the exact sum, i.e. the
+// reference's sequential f64 sum bit for bit.
+// No FP64 instruction runs per value: on this B200 the FP64 form of the same fold (F2F + DADD per
+// value) cost 5 % of the C2 forward's tensor throughput wherever it ran (score warp or epilogue).
 struct ScorePartial {
-  double s;
+  long long k;
   uint32_t e;  // emin | emax << 8 | finite << 16
   uint32_t pad;
 };
 constexpr int kPartialsPerRank = 8;  // one per epilogue warp
-// Every lane of an epilogue warp: fold its row maxima v[0..k) (rows >= L_q excluded by the caller)
-// into the warp's certified partial sum; lane 0 stores it.
-template <int K>
-MXS_DEV void store_score_partial(const float (&v)[K], const bool (&valid)[K], ScorePartial* dst, uint32_t lane) {
-  CertSum c;
+static_assert(sizeof(ScorePartial) == 16, "partial layout");
+MXS_DEV long long warp_sum_i64(long long x) {
 #pragma unroll
-  for (int i = 0; i < K; ++i)
-    if (valid[i]) c.add(v[i]);
-  c.warp_reduce();
-  if (lane == 0) *dst = ScorePartial{c.s, (uint32_t)c.emin | ((uint32_t)c.emax << 8) | ((c.finite ? 1u : 0u) << 16), 0u};
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+// Every lane of an epilogue warp: fold its row maxima v[0..K) (rows >= L_q excluded by the caller)
+// into the warp's partial; lane 0 stores it.
+template <int K>
+MXS_DEV void store_score_partial(const float (&v)[K], const bool (&valid)[K], ScorePartial* dst, uint32_t lane,
+                                 int n_values) {
+  int emin = 255, emax = 0;
+  bool fin = true;
+  uint32_t bits[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    bits[i] = valid[i] ? __float_as_uint(v[i]) : 0u;
+    exp_range(bits[i], emin, emax, fin);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  const int S = fix_shift(n_values);  // the document's L_q fixes the unit for every partial
+  long long k = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) k += fix_term(bits[i], emax, S);
+  k = warp_sum_i64(k);
+  if (lane == 0) *dst = ScorePartial{k, (uint32_t)emin | ((uint32_t)emax << 8) | ((fin ? 1u : 0u) << 16), 0u};
+}
+// Whole warp (the score warp): combine np <= 32 partials into the S4 score; `fallback` gives the
+// sequential chain when the certificate fails (or every value is +-0, whose sign only the chain
+// reproduces).
+template <typename Fallback>
+MXS_DEV double combine_score_partials(const ScorePartial* part, int np, int n_values, Fallback fallback) {
+  const int lane = (int)(threadIdx.x & 31u);
+  long long k = 0;
+  int emin = 255, emax = 0;
+  bool fin = true;
+  if (lane < np) {
+    const ScorePartial e = part[lane];
+    k = e.k;
+    emin = (int)(e.e & 0xffu);
+    emax = (int)((e.e >> 8) & 0xffu);
+    fin = (e.e >> 16) & 1u;
+  }
+  int gmin = emin, gmax = emax;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+    gmax = max(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  if (!certified(gmin, gmax, fin, n_values)) return fallback();
+  const long long total = warp_sum_i64(emax ? (k >> (gmax - emax)) : 0ll);  // exact re-basing (see above)
+  // total * 2^(gmax - 150 - S): the int64 -> f64 conversion is exact (the certificate makes the sum
+  // representable) and the scale is a power of two
+  return fix_to_double(total, gmax, fix_shift(n_values));
 }
 
 // PART = false: the score warp folds the L_q row maxima itself; PART = true: every epilogue warp
@@ -305,17 +365,8 @@ MXS_DEV void fused_score_warp(const FwdTcParams& p, uint64_t* sready, uint64_t* 
       }
       double sc;
       if constexpr (PART) {
-        const ScorePartial* part = sPart + sb * CL * kPartialsPerRank;
-        CertSum c;
-        if (lane < (uint32_t)(CL * kPartialsPerRank)) {
-          const ScorePartial e = part[lane];
-          c.s = e.s;
-          c.emin = (int)(e.e & 0xffu);
-          c.emax = (int)((e.e >> 8) & 0xffu);
-          c.finite = (e.e >> 16) & 1u;
-        }
-        c.warp_reduce();
-        sc = c.exact(p.l_q) ? c.s : warp_score_sum(buf, p.l_q);  // the latter: the sequential chain
+        sc = combine_score_partials(sPart + sb * CL * kPartialsPerRank, CL * kPartialsPerRank, p.l_q,
+                                    [&]() { return warp_score_sum(buf, p.l_q); });  // fallback: the sequential chain
       } else {
         sc = p.debug == 7 ? 0.0 : warp_score_sum(buf, p.l_q);  // 7: profiling, no sum
       }

@@ -144,18 +144,22 @@ MXS_DEV void vr_sum_warp(const VarlenRowsParams& p, long long n_emit) {
     mbar_wait_idle(&vr_ring.full[s], gen & 1u);
     const float m = vr_ring.m[s][lane];
     const long long doc = vr_ring.doc[s];
-    CertSum c;
-    if (valid) c.add(m);
-    int fin = c.finite ? 1 : 0;
+    // certified exact sum in integer fixed point (score_sum.cuh), per segment of seg lanes
+    const uint32_t bits = valid ? __float_as_uint(m) : 0u;
+    int emin = 255, emax = 0;
+    bool finb = true;
+    exp_range(bits, emin, emax, finb);
+    int fin = finb ? 1 : 0;
     for (int o = seg >> 1; o; o >>= 1) {  // segmented butterfly: xor offsets < seg stay in the segment
-      c.s += __shfl_xor_sync(0xffffffffu, c.s, o);
-      c.emin = min(c.emin, __shfl_xor_sync(0xffffffffu, c.emin, o));
-      c.emax = max(c.emax, __shfl_xor_sync(0xffffffffu, c.emax, o));
+      emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+      emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
       fin = min(fin, __shfl_xor_sync(0xffffffffu, fin, o));
     }
-    c.finite = fin != 0;
-    const bool ex = c.exact(seg);
-    double sc = c.s;
+    const bool ex = certified(emin, emax, fin != 0, seg);
+    const int S = fix_shift(seg);
+    long long k = fix_term(bits, emax, S);
+    for (int o = seg >> 1; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    double sc = fix_to_double(k, emax, S);
     if (__any_sync(0xffffffffu, lead && !ex)) {  // sequential chain (rare): the reference order
       double t = 0.0;
       for (int i = 0; i < seg; ++i) {
