@@ -661,11 +661,12 @@ def test_gather_rows_written_exactly_once(monkeypatch, dtype, dim):
 
 
 @pytest.mark.parametrize("knob,value", [("MXS_FWD_IMPL", "ss"), ("MXS_RERANK_IMPL", "r3"), ("MXS_FWD_IMPL", "ts"),
-                                        ("MXS_FWD_IMPL", "pair")])
+                                        ("MXS_FWD_IMPL", "pair"), ("MXS_PAIR_SS", "1"), ("MXS_PAIR_CL", "4")])
 def test_alternate_forward_kernels_vs_oracle(monkeypatch, knob, value):
     """The SS-form kernel (fwd_tc: Q streamed through shared memory instead of resident in TMEM),
-    the three-slot rerank kernel, the single-CTA TS kernel (fwd_ts) and the CTA-pair kernel
-    (fwd_pair) on bf16, forced by their run-time knobs on the ColPali pair shape, a 2-pair-cluster
+    the three-slot rerank kernel, the single-CTA TS kernel (fwd_ts), the CTA-pair kernel (fwd_pair)
+    and its all-shared-memory-Q (four slots) and 4-CTA-cluster variants on bf16, forced by their
+    run-time knobs on the ColPali pair shape, a 2-pair-cluster
     ragged shape, a 1-pair shape and a ragged ColBERT shape: scores within 1e-3 of the oracle,
     clear-gap argmax exact, rerank bits equal to the argmax mode."""
     monkeypatch.setenv(knob, value)
