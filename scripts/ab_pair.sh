@@ -1,7 +1,9 @@
-# C2 +argmax forward: hybrid pair (QB=4, 2 SS blocks) vs TMEM-only pairs (4-CTA clusters, 132 SMs) vs fwd_ts
+# split-Q pair mode (two independent cluster groups, TMEM-only pairs) vs the hybrid pair
+MXS_PAIR_SPLIT=1 timeout 200 python scripts/probe_pair.py 2>&1 | grep -E "AGREE|MISMATCH"
+MXS_PAIR_SPLIT=1 timeout 600 python -m pytest tests -m gpu -q -x -k "fused or acceptance or alternate or certificate or c3" 2>&1 | tail -1
 for i in 1 2; do
-ARGMAX=1 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/pair-hybrid /"
-MXS_PAIR_CL=4 ARGMAX=1 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/pair-cl4 /"
-MXS_FWD_IMPL=ts ARGMAX=1 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/ts /"
-MXS_PAIR_CL=4 ARGMAX=0 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/pair-cl4 /"
+ARGMAX=0 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/hybrid /"
+MXS_PAIR_SPLIT=1 ARGMAX=0 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/split /"
+ARGMAX=1 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/hybrid /"
+MXS_PAIR_SPLIT=1 ARGMAX=1 ROWMAX=0 timeout 60 python scripts/probe_perf.py | sed "s/^/split /"
 done
