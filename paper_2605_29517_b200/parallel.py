@@ -11,9 +11,12 @@ Shards are balanced by token count (`shard_bounds`), so the varlen corpus splits
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
+from . import _dev, _lib
 from .topk import merge_topk_across_ranks, topk
 
 
@@ -81,6 +84,39 @@ class DeviceKernels:
         off = torch.arange(b_local, dtype=torch.int64, device=D.device) * l_pad
         return _grad_query(D.reshape(b_local * l_pad, dim).contiguous(), off, argmax, g, dim)
 
+    @staticmethod
+    def csr(argmax, l_pad):
+        """The inverse CSR of the saved argmax alone (K6), so it can run beside the loss and dQ."""
+        from .backward import csr_tensors
+
+        b_local = argmax.shape[1]
+        off = torch.arange(b_local, dtype=torch.int64, device=argmax.device) * l_pad
+        lens = torch.full((b_local,), l_pad, dtype=torch.int64, device=argmax.device)
+        row_ptr, col_idx, _ = csr_tensors(argmax, off, lens, b_local * l_pad, l_pad)
+        return row_ptr, col_idx
+
+    @staticmethod
+    def grad_docs_csr(Q, argmax, g, csr, l_pad):
+        """dD from a prebuilt CSR (K7)."""
+        n_q, b_local, l_q = argmax.shape
+        dim = Q.shape[-1]
+        row_ptr, col_idx = csr
+        dD = torch.empty((b_local * l_pad, dim), dtype=torch.float32, device=Q.device)
+        _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(row_ptr), _dev.ptr(col_idx), b_local * l_pad,
+                  _dev.ptr(g), _dev.ptr(Q), n_q, b_local, l_q, dim, _dev.ptr(dD), _dev.stream_handle())
+        return dD
+
+
+_SIDE_STREAMS = {}
+
+
+def _side_stream(device):
+    """One cached side stream per device (the CSR build runs there, beside the loss and dQ)."""
+    key = torch.device(device).index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _SIDE_STREAMS[key]
+
 
 def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=None, valid_lens=None,
                  kernels=DeviceKernels):
@@ -95,6 +131,16 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     import torch.distributed as dist
 
     scores_local, argmax = kernels.score(Q, D_local, valid_lens)
+    b_local, l_pad, dim = D_local.shape
+    # the inverse CSR needs only the argmax: build it on a side stream while the loss and dQ run
+    # (a latency-bound kernel next to two bandwidth-bound ones)
+    csr = None
+    if hasattr(kernels, "csr") and argmax.is_cuda and os.environ.get("MXS_C3_OVERLAP", "1") != "0":
+        main, side = torch.cuda.current_stream(argmax.device), _side_stream(argmax.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            csr = kernels.csr(argmax, l_pad)
+        argmax.record_stream(side)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world > 1:
         parts = [torch.empty_like(scores_local) for _ in range(world)]
@@ -103,12 +149,17 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     else:
         scores = scores_local
     loss, g_full = softmax_ce(scores)
-    b_local, l_pad, dim = D_local.shape
     g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
     # dQ first: its all_reduce (NCCL, async) crosses NVLink while the dD gather kernel runs
     dQ = kernels.grad_query(D_local, argmax, g)
     work = dist.all_reduce(dQ, group=group, async_op=True) if world > 1 else None
-    dD = kernels.grad_docs(Q.to(D_local.dtype).contiguous(), argmax, g, l_pad)
+    if csr is not None:
+        main.wait_stream(side)
+        for t in csr:
+            t.record_stream(main)
+        dD = kernels.grad_docs_csr(Q.to(D_local.dtype).contiguous(), argmax, g, csr, l_pad)
+    else:
+        dD = kernels.grad_docs(Q.to(D_local.dtype).contiguous(), argmax, g, l_pad)
     if work is not None:
         work.wait()
     return loss, scores, dQ, dD.reshape(b_local, l_pad, dim)
