@@ -15,6 +15,26 @@ from . import _dev, _lib
 from .backward import csr_tensors
 
 
+_SIDE_STREAMS = {}
+
+
+def _side_stream(device):
+    """One cached side stream per device (inverse-CSR builds run there, beside the dQ gather)."""
+    key = torch.device(device).index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _SIDE_STREAMS[key]
+
+
+def _grad_docs_from_csr(Q, argmax, g, csr, n_dest, dim):
+    row_ptr, col_idx = csr
+    n_q, b, l_q = argmax.shape
+    dD = torch.empty((n_dest, dim), dtype=torch.float32, device=Q.device)
+    _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(row_ptr), _dev.ptr(col_idx), n_dest, _dev.ptr(g),
+              _dev.ptr(Q), n_q, b, l_q, dim, _dev.ptr(dD), _dev.stream_handle())
+    return dD
+
+
 def _grad_docs(Q, argmax, g, dest_off, dest_len, n_dest, max_len, dim):
     row_ptr, col_idx, _ = csr_tensors(argmax, dest_off, dest_len, n_dest, max_len)
     n_q, b, l_q = argmax.shape
@@ -52,13 +72,28 @@ class MaxSimFunction(torch.autograd.Function):
         Qc = Q.detach().to(D.dtype).contiguous()
         Dc = D.detach().contiguous()
         dQ = dD = None
+        off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
+        csr = None
+        if ctx.needs_input_grad[1] and ctx.needs_input_grad[0]:
+            # the inverse CSR (latency-bound) builds on a side stream while the dQ gather runs
+            lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
+            main, side = torch.cuda.current_stream(D.device), _side_stream(D.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                csr = csr_tensors(argmax, off, lens, b * l_pad, l_pad)[:2]
+            argmax.record_stream(side)
         if ctx.needs_input_grad[0]:
-            off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
             dQ = _grad_query(Dc.reshape(b * l_pad, dim), off, argmax, g, dim).to(Q.dtype)
         if ctx.needs_input_grad[1]:
-            off = torch.arange(b, dtype=torch.int64, device=D.device) * l_pad
-            lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
-            dD = _grad_docs(Qc, argmax, g, off, lens, b * l_pad, l_pad, dim).reshape(b, l_pad, dim).to(D.dtype)
+            if csr is not None:
+                main.wait_stream(side)
+                for t in csr:
+                    t.record_stream(main)
+                dD = _grad_docs_from_csr(Qc, argmax, g, csr, b * l_pad, dim)
+            else:
+                lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
+                dD = _grad_docs(Qc, argmax, g, off, lens, b * l_pad, l_pad, dim)
+            dD = dD.reshape(b, l_pad, dim).to(D.dtype)
         return dQ, dD, None, None, None
 
 

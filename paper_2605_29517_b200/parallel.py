@@ -16,7 +16,6 @@ import os
 import numpy as np
 import torch
 
-from . import _dev, _lib
 from .topk import merge_topk_across_ranks, topk
 
 
@@ -98,24 +97,9 @@ class DeviceKernels:
     @staticmethod
     def grad_docs_csr(Q, argmax, g, csr, l_pad):
         """dD from a prebuilt CSR (K7)."""
-        n_q, b_local, l_q = argmax.shape
-        dim = Q.shape[-1]
-        row_ptr, col_idx = csr
-        dD = torch.empty((b_local * l_pad, dim), dtype=torch.float32, device=Q.device)
-        _lib.call("mxs_grad_docs_csr", _dev.dtype_code(Q), _dev.ptr(row_ptr), _dev.ptr(col_idx), b_local * l_pad,
-                  _dev.ptr(g), _dev.ptr(Q), n_q, b_local, l_q, dim, _dev.ptr(dD), _dev.stream_handle())
-        return dD
+        from .autograd import _grad_docs_from_csr
 
-
-_SIDE_STREAMS = {}
-
-
-def _side_stream(device):
-    """One cached side stream per device (the CSR build runs there, beside the loss and dQ)."""
-    key = torch.device(device).index
-    if key not in _SIDE_STREAMS:
-        _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
-    return _SIDE_STREAMS[key]
+        return _grad_docs_from_csr(Q, argmax, g, csr, argmax.shape[1] * l_pad, Q.shape[-1])
 
 
 def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=None, valid_lens=None,
@@ -136,6 +120,8 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
     # (a latency-bound kernel next to two bandwidth-bound ones)
     csr = None
     if hasattr(kernels, "csr") and argmax.is_cuda and os.environ.get("MXS_C3_OVERLAP", "1") != "0":
+        from .autograd import _side_stream
+
         main, side = torch.cuda.current_stream(argmax.device), _side_stream(argmax.device)
         side.wait_stream(main)
         with torch.cuda.stream(side):
