@@ -63,10 +63,10 @@ struct PrSmemHeader {
 };
 
 // dynamic smem: SS Q blocks (QB = 4: 2 blocks x KA atoms of 128 rows x 128 B) | document
-// half-tile ring | argmax stash (QB blocks x 128 rows x 32 floats) | fused-score row buffers
+// half-tile ring | argmax stash (QB blocks x 128 rows x kStashPadStride floats) | fused-score row buffers
 __host__ __device__ inline size_t fwd_pair_smem_bytes(int ka, int qb, int nts, int stages, bool stash, int sum_rows) {
   return 1024 + (size_t)(qb - nts) * ka * kAtomBytes + (size_t)stages * ka * kPrHalfAtom +
-         (stash ? (size_t)qb * 128 * 128 : 0) + (size_t)kPrScoreBufs * sum_rows * sizeof(float) +
+         (stash ? (size_t)qb * 128 * kStashPadStride * sizeof(float) : 0) + (size_t)kPrScoreBufs * sum_rows * sizeof(float) +
          (sum_rows ? (size_t)kPrScoreBufs * 4 * kPartialsPerRank * sizeof(ScorePartial) : 0);
 }
 
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint8_t* sQ = smem;  // QB = 4: SS Q blocks 2, 3
   uint8_t* sD = sQ + (size_t)(QB - NTS) * KA * kAtomBytes;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kPrHalfAtom);
-  float* sSum = sBest + (p.argmax ? (size_t)QB * 128 * 32 : 0);
+  float* sSum = sBest + (p.argmax ? (size_t)QB * 128 * kStashPadStride : 0);
   ScorePartial* sPart = reinterpret_cast<ScorePartial*>(sSum + (size_t)kPrScoreBufs * p.sum_rows);
   const bool fuse = p.scores != nullptr && p.debug != 3;
   __shared__ PrSmemHeader pr_hdr;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int quad = (int)(warp & 3);
     const int row_local = quad * 32 + (int)lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const int swz = (int)(lane & 7);
+    constexpr int swz = -1;  // padded argmax stash (see stash_chunk)
     const int row_bytes = p.dim * 2;
     const uint32_t qfull_leader = mapa_u32(smem_u32(&hdr->qfull), leader);
     uint32_t qeph = 0, ndoc = 0, nt = 0;  // nt: tiles drained so far (accumulator n = QB nt + mb)
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             m[i] = 0.f;
             continue;
           }
-          float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * 32 : nullptr;
+          float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * kStashPadStride : nullptr;
           uint32_t ra[32], rb[32], rc[32], rd[32];
           tmem_ld32(taddr, ra);
           tmem_ld32(taddr + 32, rb);
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           if (p.rowmax) p.rowmax[o] = m[i];
           if (p.argmax) {
             float w[32];
-            unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * 32, w, swz);
+            unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * kStashPadStride, w, swz);
             p.argmax[o] = ntiles ? cb[i] + first_argmax32_chain(w, m[i]) : 0;  // 0: empty (invalid) doc
           }
         }

@@ -81,16 +81,21 @@ __host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, 
 
 // Stash layout: 32 floats (8 x 16 B) per (Q block, row); 16-byte pieces XOR-swizzled by lane so
 // that a warp's predicated stores spread over all banks.
+// swz < 0 (a compile-time constant at the call site): padded layout instead -- rows 144 B apart
+// (kStashPadStride floats), which is bank-conflict free for STS.128 and needs no per-store address
+// arithmetic (immediate offsets; the XOR form cost ~3 integer instructions per store).
+constexpr int kStashPadStride = 36;
 MXS_DEV void stash_chunk(float* row128, const float (&v)[32], int swz) {
   float4* dst = reinterpret_cast<float4*>(row128);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dst[i ^ swz] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  for (int i = 0; i < 8; ++i)
+    dst[swz < 0 ? i : (i ^ swz)] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 MXS_DEV void unstash_chunk(const float* row128, float (&v)[32], int swz) {
   const float4* src = reinterpret_cast<const float4*>(row128);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float4 t = src[i ^ swz];
+    const float4 t = src[swz < 0 ? i : (i ^ swz)];
     v[4 * i] = t.x;
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
