@@ -70,11 +70,11 @@ MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
 
 
 // dynamic shared memory (the header is static shared memory): document-tile ring | argmax stash
-// (`stash`: 32 floats per Q row) | INT8 scale ring (`scales`, or reserved when `bias`) | INT8 bias
+// (`stash`: kStashPadStride = 36 floats per Q row) | INT8 scale ring (`scales`, or reserved when `bias`) | INT8 bias
 // tile (`bias`) | fused-score row buffers (2 x `sum_rows` floats)
 __host__ __device__ inline size_t fwd_ts_smem_bytes(int ka, int qb, int stages, bool scales, bool bias, bool stash,
                                                     int sum_rows) {
-  return 1024 + (size_t)stages * ka * kAtomBytes + (stash ? (size_t)qb * 128 * 128 : 0) +
+  return 1024 + (size_t)stages * ka * kAtomBytes + (stash ? (size_t)qb * 128 * 36 * 4 : 0) +
          ((scales || bias) ? (size_t)kScaleSlots * kTileRows * sizeof(float) : 0) + (bias ? kBiasTileBytes : 0) +
          (size_t)2 * sum_rows * sizeof(float);
 }
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint8_t* sD = smem;
   float* sBest = reinterpret_cast<float*>(sD + (size_t)p.stages * KA * kAtomBytes);
   // INT8 scale ring (only when d_scale rows are 16-B aligned: l_pad % 4 == 0)
-  float* sScale = sBest + (p.argmax ? (size_t)p.qb * 128 * 32 : 0);
+  float* sScale = sBest + (p.argmax ? (size_t)p.qb * 128 * kStashPadStride : 0);
   const bool scale_ring = (KIND == TcKind::I8) && ((p.l_pad & 3) == 0);
   // INT8 with |acc| <= 2^22 (d <= 256): accumulators pre-biased to kMagicF (see fill_bias_tile)
   constexpr bool kBias = (KIND == TcKind::I8) && (KA <= 2);
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int quad = (int)(warp & 3);
     const int row_local = quad * 32 + (int)lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const int swz = (int)(lane & 7);
+    constexpr int swz = -1;  // padded argmax stash (see stash_chunk)
     const int eb = (KIND == TcKind::I8) ? 1 : 2;
     const int row_bytes = p.dim * eb;
     uint32_t sph = 0, qeph = 0;  // this set's slot is `wset`; sph = parity of its next use
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(kTsAccCol0 + slot * 128);
           // argmax not requested (rerank: scores only) -> no index tracking at all
-          float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * 32 : nullptr;
+          float* stash = p.argmax ? sBest + ((size_t)mb * 128 + row_local) * kStashPadStride : nullptr;
           const int base = t * kTileRows;
           if (p.debug == 2) {  // profiling knob: drain the slot without folding
             tc_fence_before();
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           if (p.rowmax) p.rowmax[obase + row] = m[i];
           if (p.argmax) {
             float w[32];
-            unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * 32, w, swz);
+            unstash_chunk(sBest + ((size_t)mb * 128 + row_local) * kStashPadStride, w, swz);
             p.argmax[obase + row] = ntiles ? cb[i] + first_argmax32_chain(w, m[i]) : 0;  // 0: empty (invalid) doc
           }
         }
