@@ -33,9 +33,6 @@
 
 namespace mxs {
 
-#ifndef MXS_PR_WARP_ARRIVE
-#define MXS_PR_WARP_ARRIVE 0  // 1: one fused-score arrive per epilogue warp instead of per lane
-#endif
 constexpr int kPrMaxSlots = 4;
 #ifndef MXS_PR_SCORE_BUFS
 #define MXS_PR_SCORE_BUFS 2
@@ -167,7 +164,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     mbar_init(&hdr->qsfull, 1);             // leader: its TMA warp's expect_tx arrive
     mbar_init(&hdr->qempty, 1);
     for (int s = 0; s < kPrScoreBufs; ++s) {
-      mbar_init(&hdr->sready[s], MXS_PR_WARP_ARRIVE ? kEpiWarps : 32 * kEpiWarps);
+      mbar_init(&hdr->sready[s], 32 * kEpiWarps);
       mbar_init(&hdr->sfree[s], 1);
       mbar_init(&hdr->speer[s], 1);  // rank 0's expect_tx arrive + the other ranks' bulk-copy bytes
       mbar_init(&hdr->sdone[s], 1);
@@ -336,12 +333,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
                                    lane, p.l_q);
         }
         if (p.debug != 8) fence_proxy_async();  // rows + partial travel to cluster rank 0 by bulk (async-proxy) copy
-#if MXS_PR_WARP_ARRIVE
-        __syncwarp();  // orders every lane's stores before lane 0's release-arrive
-        if (lane == 0) mbar_arrive(&hdr->sready[pend_sb]);
-#else
-        if (p.debug != 6 && p.debug < 8) mbar_arrive(&hdr->sready[pend_sb]);
-#endif
+        if (p.debug != 6 && p.debug < 8) mbar_arrive(&hdr->sready[pend_sb]);  // every lane (release of its stores)
         pend_sb = -1;
       }
     };

@@ -245,24 +245,10 @@ MXS_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 
 // Rows [r0, r1) of rank r's share of a fused-score row buffer, padded to whole 16-byte chunks
 // (the buffers hold whole 128-row blocks, so the padding stays inside them).
 MXS_DEV uint32_t score_rows_bytes(int r0, int r1) { return (uint32_t)(((r1 - r0) + 3) & ~3) * 4u; }
-#ifndef MXS_SCORE_WAIT_SPIN
-#define MXS_SCORE_WAIT_SPIN 0  // 1: the score warps spin on their barriers instead of suspending
-#endif
-MXS_DEV void score_wait(uint64_t* bar, uint32_t parity) {
-#if MXS_SCORE_WAIT_SPIN
-  mbar_wait(bar, parity);
-#else
-  mbar_wait_idle(bar, parity);
-#endif
-}
-MXS_DEV void score_wait_cluster(uint64_t* bar, uint32_t parity) {
-#if MXS_SCORE_WAIT_SPIN
-  mbar_wait_cluster(bar, parity);
-#else
-  mbar_wait_cluster_idle(bar, parity);
-#endif
-}
-// Certified partial sum of one epilogue warp's row maxima (PART mode of fused_score_warp): 16 bytes.
+// The score warps mostly wait: suspending waits keep them off the epilogue warps' issue slots
+// (spinning measured the same).
+MXS_DEV void score_wait(uint64_t* bar, uint32_t parity) { mbar_wait_idle(bar, parity); }
+MXS_DEV void score_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait_cluster_idle(bar, parity); }
 // Certified partial of one epilogue warp's row maxima (PART mode of fused_score_warp), 16 bytes, in
 // INTEGER fixed point: k = sum of the values in units of 2^(emax - 150 - S) (emax = the warp's
 // largest biased exponent, S = 29 - ceil(log2 L_q)), plus the exponent range and finiteness for the
