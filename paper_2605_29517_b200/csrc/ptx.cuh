@@ -248,8 +248,9 @@ MXS_DEV float fmin3(float a, float b, float c) {
 }
 // Packed fp32 pair multiply (FMUL2), round-to-nearest: {a.x*b.x, a.y*b.y}.
 // NOTE: ptxas (12.9) contracts mul.rn.f32x2 followed by a dependent add.rn.f32x2 into FFMA2 despite
-// the explicit rounding modifiers (observed in SASS); never feed an fmul2_rn result into fadd2_rn
-// where two roundings are required -- use scalar __fmul_rn / __fadd_rn there.
+// the explicit rounding modifiers (observed in SASS) -- and also fma.rn.f32x2(a, b, -0) followed by
+// add.rn.f32x2 (it folds the -0 addend, then contracts); never feed a packed product into a packed
+// add where two roundings are required -- use scalar __fmul_rn / __fadd_rn there.
 MXS_DEV void fmul2_rn(float& o0, float& o1, float a0, float a1, float b0, float b1) {
   unsigned long long a, b, d;
   asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
