@@ -169,13 +169,10 @@ MXS_DEV void ts_chunk(const uint32_t (&r)[32], int base, int vl, const FwdTcPara
     m = fmaxf(m, cmax);
     return;
   }
-  const bool upd = cmax > m;
-  if (__any_sync(0xffffffffu, upd)) {
-    if (upd) {
-      m = cmax;
-      cb = base;
-      stash_chunk(stash_row, v, swz);
-    }
+  if (cmax > m) {  // predicated stash (see ts_chunk_full)
+    m = cmax;
+    cb = base;
+    stash_chunk(stash_row, v, swz);
   }
 }
 
@@ -212,13 +209,12 @@ MXS_DEV void ts_chunk_full(const uint32_t (&r)[32], int base, float sq, float& m
   if constexpr (!kArgmax) {
     m = fmaxf(m, cmax);
   } else {
-    const bool upd = cmax > m;
-    if (__any_sync(0xffffffffu, upd)) {
-      if (upd) {
-        m = cmax;
-        cb = base;
-        stash_chunk(stash_row, v, swz);
-      }
+    // improving lanes stash their chunk (predicated stores; guarding them with a warp vote and a
+    // branch was 5 % slower at C2 +argmax -- nearly every chunk has an improving lane)
+    if (cmax > m) {
+      m = cmax;
+      cb = base;
+      stash_chunk(stash_row, v, swz);
     }
   }
 }
