@@ -293,15 +293,27 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* 
   long long* sv_i = reinterpret_cast<long long*>(sv_s + kSelSurvivors);
   const long long lo = (long long)blockIdx.x * chunk;
   const int m = (int)max(0LL, min(n, lo + chunk) - lo);
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    const double v = in_s[lo + e];
-    if (in_ids) {
+  // the slice -> shared memory with many loads in flight per thread (a dependent load -> store
+  // loop paid one L2 round trip per element and dominated the kernel)
+  if (in_ids) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+      const double v = in_s[lo + e];
       const long long i = in_ids[lo + e];
       ss[e] = (i >= 0) ? v : kNaN;
       si[e] = i;
-    } else {
-      ss[e] = v;
     }
+  } else {
+    const double* src = in_s + lo;
+    int e = threadIdx.x;
+    for (; e + 7 * (int)blockDim.x < m; e += 8 * (int)blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + e + u * (int)blockDim.x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ss[e + u * (int)blockDim.x] = v[u];
+    }
+    for (; e < m; e += blockDim.x) ss[e] = __ldg(src + e);
   }
   __syncthreads();
   double* os = out_s + (long long)blockIdx.x * k;
