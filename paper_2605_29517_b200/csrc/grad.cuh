@@ -345,7 +345,12 @@ struct Vec16<float> {
 #ifndef GRAD_LOAD
 #define GRAD_LOAD(p) __ldg(reinterpret_cast<const uint4*>(p))
 #endif
-constexpr int kGradGU = MXS_GRAD_GU;  // source rows per lane group and step
+constexpr int kGradGU = MXS_GRAD_GU;  // source rows per lane group and step (dD)
+// dQ (K8) keeps twice as many rows in flight: 81 vs 86 us at C3, where dD runs slower with 16
+// (88 vs 82 us) -- scripts/ab_grad.sh
+#ifndef MXS_GRAD_GU_Q
+#define MXS_GRAD_GU_Q 16
+#endif
 constexpr int kGradWarps = 8;  // warps per block of the row-group kernels
 
 // Per-warp staging of one chunk of up to 32 sources: (gathered row, weight), written once by the
@@ -397,21 +402,22 @@ MXS_DEV void unpack16<float>(const uint4& t, float (&o)[4]) {
 // One step = kGradGU source rows per lane group.  Latency is hidden by occupancy (32-40
 // registers, 64 warps per SM), not by deeper per-warp pipelining: a software-pipelined variant
 // (two steps in flight, 70 registers) measured 126 us vs 87 us at C3 (scripts/probe_grad.py).
-template <typename T, int LPR>
+template <typename T, int LPR, int GU = kGradGU>
 MXS_DEV void grad_rowgroup_chunk(const T* __restrict__ base, int dim, const GradStage& st, int n,
                                  float (&acc)[Vec16<T>::N], int h, int lp) {
   constexpr int V = Vec16<T>::N, SP = 32 / LPR;
-  for (int j0 = 0; j0 < n; j0 += SP * kGradGU) {
-    uint4 raw[kGradGU];
-    float ws[kGradGU];
+  constexpr int G = (SP * GU > 32) ? 32 / SP : GU;  // one step never reaches past the 32 staged sources
+  for (int j0 = 0; j0 < n; j0 += SP * G) {
+    uint4 raw[G];
+    float ws[G];
 #pragma unroll
-    for (int u = 0; u < kGradGU; ++u) {
+    for (int u = 0; u < G; ++u) {
       const int j = j0 + u * SP + h;  // entries past n hold (row 0, weight 0)
       ws[u] = st.w[j & 31];
       raw[u] = GRAD_LOAD(base + (long long)st.row[j & 31] * dim + lp * V);
     }
 #pragma unroll
-    for (int u = 0; u < kGradGU; ++u) {
+    for (int u = 0; u < G; ++u) {
       float x[V];
       unpack16<T>(raw[u], x);
 #pragma unroll
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(32 * kGradWarps) grad_query_rg_kernel(const T*
     st.row[lane] = my_row;
     st.w[lane] = my_w;
     __syncwarp();
-    grad_rowgroup_chunk<T, LPR>(D, p.dim, st, n, acc, h, lp);
+    grad_rowgroup_chunk<T, LPR, MXS_GRAD_GU_Q>(D, p.dim, st, n, acc, h, lp);
   }
   note_row_write(p, wq, lane);
   grad_rowgroup_store<T, LPR>(acc, p.dQ + wq * p.dim, lane);
