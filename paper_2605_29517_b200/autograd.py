@@ -79,17 +79,18 @@ class MaxSimFunction(torch.autograd.Function):
             lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
             main, side = torch.cuda.current_stream(D.device), _side_stream(D.device)
             side.wait_stream(main)
+            # ... and the dD gather follows it there, concurrent with dQ (C3 step 0.972 -> 0.957 ms)
             with torch.cuda.stream(side):
                 csr = csr_tensors(argmax, off, lens, b * l_pad, l_pad)[:2]
-            argmax.record_stream(side)
+                dD = _grad_docs_from_csr(Qc, argmax, g, csr, b * l_pad, dim)
+            for t in (argmax, Qc, g):
+                t.record_stream(side)
         if ctx.needs_input_grad[0]:
             dQ = _grad_query(Dc.reshape(b * l_pad, dim), off, argmax, g, dim).to(Q.dtype)
         if ctx.needs_input_grad[1]:
             if csr is not None:
                 main.wait_stream(side)
-                for t in csr:
-                    t.record_stream(main)
-                dD = _grad_docs_from_csr(Qc, argmax, g, csr, b * l_pad, dim)
+                dD.record_stream(main)
             else:
                 lens = torch.full((b,), l_pad, dtype=torch.int64, device=D.device)
                 dD = _grad_docs(Qc, argmax, g, off, lens, b * l_pad, l_pad, dim)

@@ -136,10 +136,22 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
         scores = scores_local
     loss, g_full = softmax_ce(scores)
     g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
+    dD = None
+    if csr is not None and os.environ.get("MXS_C3_CONCURRENT", "1") != "0":
+        # dD on the side stream right behind its CSR, concurrent with dQ on the main stream: the
+        # two L2 gathers share the GPU instead of each paying its own tail
+        side.wait_stream(main)  # g (the loss) is ready
+        with torch.cuda.stream(side):
+            dD = kernels.grad_docs_csr(Q.to(D_local.dtype).contiguous(), argmax, g, csr, l_pad)
+        g.record_stream(side)
+        Q.record_stream(side)
     # dQ first: its all_reduce (NCCL, async) crosses NVLink while the dD gather kernel runs
     dQ = kernels.grad_query(D_local, argmax, g)
     work = dist.all_reduce(dQ, group=group, async_op=True) if world > 1 else None
-    if csr is not None:
+    if dD is not None:
+        main.wait_stream(side)
+        dD.record_stream(main)
+    elif csr is not None:
         main.wait_stream(side)
         for t in csr:
             t.record_stream(main)
