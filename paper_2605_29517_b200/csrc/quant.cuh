@@ -88,6 +88,27 @@ MXS_DEV float quant_round_fast(float x, float s, float r) {
   return t;
 }
 
+// The same rounding for a pair, without FRND / F2I: z = fl(y + 1.5 * 2^23) rounds y to the
+// nearest integer, ties to even (exactly rintf for |y| < 2^22), and z's bit pattern is
+// 0x4B400000 + rint(y), whose low byte is rint(y) as an int8 (|rint(y)| <= 127 here).  The
+// half-integer check uses t = z - 1.5 * 2^23 (exact).  Packed FMUL2 / FADD2 on the FMA pipe
+// instead of FRND + F2I per element.
+MXS_DEV void quant_round_magic2(uint32_t& o0, uint32_t& o1, float x0, float x1, float s, float r) {
+  constexpr float kM = 12582912.0f;  // 1.5 * 2^23
+  float y0, y1, z0, z1, t0, t1, d0, d1;
+  fmul2_rn(y0, y1, x0, x1, r, r);
+  fadd2_rn(z0, z1, y0, y1, kM, kM);
+  fadd2_rn(t0, t1, z0, z1, -kM, -kM);
+  fadd2_rn(d0, d1, y0, y1, -t0, -t1);
+  o0 = __float_as_uint(z0);
+  o1 = __float_as_uint(z1);
+  // near a half-integer (rare): the exact division decides, as in quant_round_fast.  (Collecting
+  // the flags and redoing flagged elements in one loop after the row measured slower: 0.98 vs
+  // 0.82 ms at C4.)
+  if (fabsf(d0) > 0.5f - 0x1p-12f) o0 = (uint32_t)(int)rintf(__fdiv_rn(x0, s));
+  if (fabsf(d1) > 0.5f - 0x1p-12f) o1 = (uint32_t)(int)rintf(__fdiv_rn(x1, s));
+}
+
 template <typename T, int U>
 __global__ void __launch_bounds__(256) quantize128_stream_kernel(const T* __restrict__ x, long long rows, int levels,
                                                                  int8_t* __restrict__ q, float* __restrict__ scale) {
@@ -132,11 +153,11 @@ __global__ void __launch_bounds__(256) quantize128_stream_kernel(const T* __rest
         uint32_t w[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          int t[4];
+          uint32_t t[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) t[j] = (int)quant_round_fast(v[4 * c + j], s, r);
-          w[c] = __byte_perm(__byte_perm((uint32_t)t[0], (uint32_t)t[1], 0x0040), __byte_perm((uint32_t)t[2], (uint32_t)t[3], 0x0040),
-                             0x5410);
+          for (int j = 0; j < 4; j += 2) quant_round_magic2(t[j], t[j + 1], v[4 * c + j], v[4 * c + j + 1], s, r);
+          // the low byte of each rounded value's bit pattern is its int8 two's-complement byte
+          w[c] = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
         }
         reinterpret_cast<uint4*>(q + row[u] * 128)[l8] = make_uint4(w[0], w[1], w[2], w[3]);
       }
