@@ -10,7 +10,7 @@
 #include "chamfer.cuh"
 
 #ifndef MXS_QUANT_U
-#define MXS_QUANT_U 2  // rows in flight per 8-lane group of the streaming quantiser
+#define MXS_QUANT_U 1  // rows per pass and 8-lane group of the streaming quantiser (+ the prefetched next pass)
 #endif
 #include "host.h"
 
@@ -100,7 +100,7 @@ int mxs_quantize_per_token(int dtype, const void* x, int64_t rows, int64_t dim, 
   else if ((dtype == MXS_BF16 || dtype == MXS_F16) && dim == 128 &&
            (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
     // persistent 8-lanes-per-row kernel: 8 blocks of 256 threads per SM
-    const long long want = (rows + 32 * MXS_QUANT_U - 1) / (32 * MXS_QUANT_U);  // 32 groups x U rows per block pass (U = 4: 93 regs, slower)
+    const long long want = (rows + 32 * MXS_QUANT_U - 1) / (32 * MXS_QUANT_U);  // 32 groups x U rows per block pass
     const long long sblocks = want < (long long)sm_count() * 8 ? want : (long long)sm_count() * 8;
     if (dtype == MXS_BF16)
       mxs::quantize128_stream_kernel<__nv_bfloat16, MXS_QUANT_U>

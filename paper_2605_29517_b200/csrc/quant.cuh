@@ -117,6 +117,22 @@ __global__ void __launch_bounds__(256) quantize128_stream_kernel(const T* __rest
   const long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;  // 8-lane group id
   const long long n_grp = ((long long)gridDim.x * blockDim.x) >> 3;
   const float lv = (float)levels;
+  // the next pass's rows are loaded before this pass's arithmetic (software prefetch: twice the
+  // bytes in flight per lane group)
+  auto load_rows = [&](long long r0, uint4 (&raw)[U][2]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long rr = r0 + u * n_grp;
+      raw[u][0] = raw[u][1] = make_uint4(0u, 0u, 0u, 0u);
+      if (rr < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + rr * 128) + 2 * l8;
+        raw[u][0] = __ldg(src);
+        raw[u][1] = __ldg(src + 1);
+      }
+    }
+  };
+  uint4 nxt[U][2];
+  load_rows(grp, nxt);
   for (long long r0 = grp; r0 - grp < rows; r0 += U * n_grp) {  // warp-uniform trip count
     long long row[U];
 #pragma unroll
@@ -124,13 +140,10 @@ __global__ void __launch_bounds__(256) quantize128_stream_kernel(const T* __rest
     uint4 raw[U][2];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      raw[u][0] = raw[u][1] = make_uint4(0u, 0u, 0u, 0u);
-      if (row[u] < rows) {
-        const uint4* src = reinterpret_cast<const uint4*>(x + row[u] * 128) + 2 * l8;
-        raw[u][0] = __ldg(src);
-        raw[u][1] = __ldg(src + 1);
-      }
+      raw[u][0] = nxt[u][0];
+      raw[u][1] = nxt[u][1];
     }
+    load_rows(r0 + U * n_grp, nxt);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float v[16];
