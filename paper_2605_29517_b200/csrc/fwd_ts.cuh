@@ -61,7 +61,13 @@ struct TsSmemHeader {
 // see i2f2_biased), leaving f32(acc) exactly, so the epilogue does no conversion at all.  Cost: two
 // K = 16 bf16 MMAs per accumulator (+50 % tensor-pipe time: measured raw TMA + MMA rate 0.82 ms ->
 // 1.14 ms at C4) on an epilogue-bound kernel (C4 rerank 1.61 -> 1.51 ms).
-constexpr int kBiasTileBytes = 128 * 128;  // one SW128 K-major bf16 atom, 128 rows x 128 B
+constexpr int kBiasTileBytes = 128 * 128;
+#ifndef MXS_TS_I8_PIPE
+#define MXS_TS_I8_PIPE 1  // software-pipelined INT8 argmax drain (C4 +argmax 2.476 -> 2.396 ms)
+#endif
+#ifndef MXS_TS_PIPE
+#define MXS_TS_PIPE 0  // software-pipelined bf16 / fp16 drain on full tiles (A/B)
+#endif  // one SW128 K-major bf16 atom, 128 rows x 128 B
 MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
   const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
   uint4* t4 = reinterpret_cast<uint4*>(tile);
@@ -686,6 +692,28 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           } else if (KIND == TcKind::I8 && KA <= 2 && sdt != nullptr && base + kTileRows <= vl) {
             // full tile, staged scales: straight-line chunks, argmax tracking decided at compile time
             uint32_t ra[32], rb[32];
+#if MXS_TS_I8_PIPE
+            // software-pipelined drain (as fwd_i8r): the load of chunk c + 1 is in flight while
+            // chunk c is folded; the slot is released once chunk 3 has landed
+            if (stash) {
+              tmem_ld32(taddr, ra);
+              tmem_ld_wait_regs(ra);
+              tmem_ld32(taddr + 32, rb);
+              ts_chunk_full<KIND, true, kBias>(ra, base, sq[i], m[i], cb[i], stash, swz, sdt);
+              tmem_ld_wait_regs(rb);
+              tmem_ld32(taddr + 64, ra);
+              ts_chunk_full<KIND, true, kBias>(rb, base + 32, sq[i], m[i], cb[i], stash, swz, sdt + 32);
+              tmem_ld_wait_regs(ra);
+              tmem_ld32(taddr + 96, rb);
+              ts_chunk_full<KIND, true, kBias>(ra, base + 64, sq[i], m[i], cb[i], stash, swz, sdt + 64);
+              tmem_ld_wait_regs(rb);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&hdr->tempty[slot]);
+              ts_chunk_full<KIND, true, kBias>(rb, base + 96, sq[i], m[i], cb[i], stash, swz, sdt + 96);
+              continue;
+            }
+#endif
             tmem_ld32(taddr, ra);
             tmem_ld32(taddr + 32, rb);
             tmem_ld_wait();
