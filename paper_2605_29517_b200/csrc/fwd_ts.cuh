@@ -61,13 +61,10 @@ struct TsSmemHeader {
 // see i2f2_biased), leaving f32(acc) exactly, so the epilogue does no conversion at all.  Cost: two
 // K = 16 bf16 MMAs per accumulator (+50 % tensor-pipe time: measured raw TMA + MMA rate 0.82 ms ->
 // 1.14 ms at C4) on an epilogue-bound kernel (C4 rerank 1.61 -> 1.51 ms).
-constexpr int kBiasTileBytes = 128 * 128;
+constexpr int kBiasTileBytes = 128 * 128;  // one SW128 K-major bf16 atom, 128 rows x 128 B
 #ifndef MXS_TS_I8_PIPE
 #define MXS_TS_I8_PIPE 1  // software-pipelined INT8 argmax drain (C4 +argmax 2.476 -> 2.396 ms)
 #endif
-#ifndef MXS_TS_PIPE
-#define MXS_TS_PIPE 0  // software-pipelined bf16 / fp16 drain on full tiles (A/B)
-#endif  // one SW128 K-major bf16 atom, 128 rows x 128 B
 MXS_DEV void fill_bias_tile(uint8_t* tile, int tid, int nthreads) {
   const uint4 chunk = make_uint4(0x44804500u, 0x00004480u, 0u, 0u);  // bf16 {2048, 1024 | 1024, 0 | 0, 0 | 0, 0}
   uint4* t4 = reinterpret_cast<uint4*>(tile);
