@@ -240,6 +240,22 @@ def test_quantize_random_bitwise_vs_oracle():
     assert np.array_equal(qb.cpu().numpy(), q2) and np.array_equal(sb.cpu().numpy(), s2)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_quantize_streaming_kernel_many_rows_bitwise(dtype):
+    """The persistent d = 128 streaming quantiser (magic-number rounding, next row prefetched) on
+    a row count that is not a multiple of any pass width, with zero rows and mixed scales, vs the
+    oracle: every int8 and every scale bit-identical."""
+    rng = np.random.default_rng(11)
+    n = 100_003
+    x = (rng.standard_normal((n, 128)) * rng.uniform(1e-3, 50, (n, 1))).astype(np.float32)
+    x[::997] = 0
+    x[7::1001, 3] = 127.0 * np.abs(x[7::1001]).max(axis=1)  # rows whose scale is exactly representable
+    xt = cuda(x, dtype)
+    q, sc = orc.quantize_per_token(xt.float().cpu().numpy())
+    qm, sm = mx.quant.quantize_tensor(xt)
+    assert np.array_equal(qm.cpu().numpy(), q) and np.array_equal(sm.cpu().numpy(), sc)
+
+
 def test_int8_golden_bitwise():
     g = golden("int8")
     corpus = mx.QuantizedCorpus(g["d_q"], g["d_s"])
