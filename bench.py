@@ -658,27 +658,25 @@ def run_c5(a, rank, world, local_rank, steps, warmup, cpu):
     stream = torch.cuda.current_stream()
     sh = _dev.stream_handle(stream)
     P = _dev.ptr
-    ev = ev_pair(torch)
-    kern_ms = []
+    # the varlen kernel's own launch time, recorded live around every call (the last `steps`
+    # calls are the timed region's)
+    evs = [ev_pair(torch) for _ in range(warmup + steps)]
+    n_call = [0]
 
-    def step(timed=False):
-        if timed:
-            ev[0].record(stream)
+    def step():
+        ev = evs[min(n_call[0], len(evs) - 1)]
+        n_call[0] += 1
+        ev[0].record(stream)
         _lib.call("mxs_fused_score_varlen", _lib.MXS_BF16, P(q), 1, 32, P(toks), P(cu_d), n_loc, T, 128, P(scores),
                   None, None, 0, sh)
-        if timed:
-            ev[1].record(stream)
+        ev[1].record(stream)
         _lib.call("mxs_topk", P(scores), n_loc, k, lo, P(top_s), P(top_i), P(ws), ws_bytes, sh)
         if world > 1:
             return select_candidates(*_gather(top_s, top_i, world, dist), k)
         return top_s, top_i
 
     ms = timed_loop(torch, dist, world, dev, steps, warmup, step, stream)
-    for _ in range(3):
-        step(timed=True)
-        torch.cuda.synchronize()
-        kern_ms.append(ev[0].elapsed_time(ev[1]))
-    kms = statistics.median(kern_ms)
+    kms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs[warmup:])
     shard_bytes = T * 128 * 2 + (n_loc + 1) * 8 + n_loc * 8
     gbs = torch.tensor([shard_bytes / (kms / 1e3) / 1e9], dtype=torch.float64, device=dev)
     gbs_min = gbs.clone()
