@@ -120,6 +120,15 @@ int mxs_fused_score_varlen(int dtype, const void* Q, int64_t n_q, int64_t l_q, c
                            const int64_t* cu_seqlens, int64_t n_docs, int64_t n_tokens, int64_t dim, double* scores,
                            int32_t* argmax, float* rowmax, int exact, void* stream);
 
+/*
+ * In-batch contrastive loss (positives on the diagonal) and its score gradient, fused.  Replaces
+ * maxsim/cli.py:198 _softmax_ce for the C3 training step: scores f64 [n_q, b] (b >= n_q) ->
+ * loss f64 [1] = mean_q(logsumexp(s[q]) - s[q, q]) and g f32 [n_q, ncols] = the columns
+ * [col0, col0 + ncols) of (softmax(s) - eye) / n_q.
+ */
+int mxs_softmax_ce(const double* scores, int64_t n_q, int64_t b, int64_t col0, int64_t ncols, double* loss, float* g,
+                   void* stream);
+
 /* Sequential f64 row sum (S4) of rowmax [n_pairs, l_q] into scores [n_pairs]. */
 int mxs_rowsum(const float* rowmax, int64_t n_pairs, int64_t l_q, double* scores, void* stream);
 

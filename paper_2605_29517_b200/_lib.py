@@ -32,6 +32,7 @@ _SIGNATURES = {
     "mxs_fused_rowmax_batch": [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "mxs_fused_score_int8": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "mxs_rowsum": [c_vp, c_i64, c_i64, c_vp, c_vp],
+    "mxs_softmax_ce": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp],
     "mxs_fused_score_varlen": [c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int,
                                c_vp],
     "mxs_quantize_per_token": [c_int, c_vp, c_i64, c_i64, c_int, c_vp, c_vp, c_vp],

@@ -8,6 +8,7 @@
 #include "quant.cuh"
 #include "topk.cuh"
 #include "chamfer.cuh"
+#include "loss.cuh"
 
 #ifndef MXS_QUANT_U
 #define MXS_QUANT_U 1  // rows per pass and 8-lane group of the streaming quantiser (+ the prefetched next pass)
@@ -284,3 +285,19 @@ int mxs_validate_cu_seqlens(const int64_t* cu_seqlens, int64_t n_docs, int64_t n
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int mxs_softmax_ce(const double* scores, int64_t n_q, int64_t b, int64_t col0, int64_t ncols, double* loss, float* g,
+                   void* stream) {
+  if (!scores || !loss || (!g && ncols > 0)) return fail(MXS_INVALID_ARGUMENT, "mxs_softmax_ce: null pointer");
+  if (n_q < 1 || b < n_q || col0 < 0 || ncols < 0 || col0 + ncols > b || b >= (1LL << 31))
+    return fail(MXS_SHAPE_MISMATCH, "mxs_softmax_ce: scores [%lld, %lld] with positives on the diagonal, columns "
+                "[%lld, %lld)", (long long)n_q, (long long)b, (long long)col0, (long long)(col0 + ncols));
+  mxs::softmax_ce_kernel<<<1, mxs::kLossThreads, 0, (cudaStream_t)stream>>>(scores, (int)n_q, (int)b, (int)col0,
+                                                                           (int)ncols, loss, g);
+  return check_launch("softmax_ce_kernel");
+}
+
+}  // extern "C"
+

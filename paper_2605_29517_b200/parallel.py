@@ -44,6 +44,21 @@ def sharded_topk(local_scores: torch.Tensor, k: int, doc_offset: int, group=None
     return merge_topk_across_ranks(ts, ti, k, group=group, select=select)
 
 
+def softmax_ce_device(scores: torch.Tensor, col0: int, ncols: int):
+    """`softmax_ce` fused into one kernel (mxs_softmax_ce): returns (loss f64 0-d tensor, g f32
+    [n_q, ncols] = columns [col0, col0 + ncols) of the score gradient), on the scores' device."""
+    from . import _dev, _lib
+
+    s = scores.to(torch.float64).contiguous()
+    n_q, b = s.shape
+    loss = torch.empty((), dtype=torch.float64, device=s.device)
+    g = torch.empty((n_q, ncols), dtype=torch.float32, device=s.device)
+    with _dev.on_device(s):
+        _lib.call("mxs_softmax_ce", _dev.ptr(s), n_q, b, col0, ncols, _dev.ptr(loss), _dev.ptr(g),
+                  _dev.stream_handle(None, s.device))
+    return loss, g
+
+
 def softmax_ce(scores: torch.Tensor):
     """In-batch contrastive loss with positives on the diagonal (maxsim/cli.py:198-206), float64."""
     s = scores.to(torch.float64)
@@ -54,6 +69,19 @@ def softmax_ce(scores: torch.Tensor):
     probs = torch.exp(s - lse[:, None])
     grad = (probs - torch.eye(b, dtype=s.dtype, device=s.device)) / b
     return loss, grad
+
+
+_OFFSETS = {}
+
+
+def _doc_offsets(b_local: int, l_pad: int, device):
+    """Cached (row offset, length) tensors of b_local equal-length documents (read-only; saves the
+    arange / full launches of every step)."""
+    key = (b_local, l_pad, torch.device(device))
+    if key not in _OFFSETS:
+        off = torch.arange(b_local, dtype=torch.int64, device=device) * l_pad
+        _OFFSETS[key] = (off, torch.full((b_local,), l_pad, dtype=torch.int64, device=device))
+    return _OFFSETS[key]
 
 
 class DeviceKernels:
@@ -71,8 +99,7 @@ class DeviceKernels:
         from .autograd import _grad_docs
 
         b_local = argmax.shape[1]
-        off = torch.arange(b_local, dtype=torch.int64, device=Q.device) * l_pad
-        lens = torch.full((b_local,), l_pad, dtype=torch.int64, device=Q.device)
+        off, lens = _doc_offsets(b_local, l_pad, Q.device)
         return _grad_docs(Q, argmax, g, off, lens, b_local * l_pad, l_pad, Q.shape[-1])
 
     @staticmethod
@@ -80,7 +107,7 @@ class DeviceKernels:
         from .autograd import _grad_query
 
         b_local, l_pad, dim = D.shape
-        off = torch.arange(b_local, dtype=torch.int64, device=D.device) * l_pad
+        off, _ = _doc_offsets(b_local, l_pad, D.device)
         return _grad_query(D.reshape(b_local * l_pad, dim).contiguous(), off, argmax, g, dim)
 
     @staticmethod
@@ -89,8 +116,7 @@ class DeviceKernels:
         from .backward import csr_tensors
 
         b_local = argmax.shape[1]
-        off = torch.arange(b_local, dtype=torch.int64, device=argmax.device) * l_pad
-        lens = torch.full((b_local,), l_pad, dtype=torch.int64, device=argmax.device)
+        off, lens = _doc_offsets(b_local, l_pad, argmax.device)
         row_ptr, col_idx, _ = csr_tensors(argmax, off, lens, b_local * l_pad, l_pad)
         return row_ptr, col_idx
 
@@ -134,8 +160,11 @@ def inbatch_step(Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=
         scores = torch.cat(parts, dim=1)
     else:
         scores = scores_local
-    loss, g_full = softmax_ce(scores)
-    g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
+    if scores.is_cuda and hasattr(kernels, "csr"):  # device kernels: one fused loss launch
+        loss, g = softmax_ce_device(scores, doc_offset, b_local)
+    else:
+        loss, g_full = softmax_ce(scores)
+        g = g_full[:, doc_offset : doc_offset + b_local].to(torch.float32).contiguous()
     dD = None
     if csr is not None and os.environ.get("MXS_C3_CONCURRENT", "1") != "0":
         # dD on the side stream right behind its CSR, concurrent with dQ on the main stream: the

@@ -701,3 +701,23 @@ def test_alternate_forward_kernels_vs_oracle(monkeypatch, knob, value):
         assert np.array_equal(am.cpu().numpy()[safe], ref_a[safe])
         s2, _, _ = mx.score_dense(Qr, Dr, cuda(vl), want_argmax=False)
         assert rel_err(s2.cpu().numpy(), ref_s) < REL
+
+
+@pytest.mark.parametrize("n,col0,ncols", [(64, 0, 64), (64, 16, 32), (7, 3, 4), (300, 100, 200)])
+def test_fused_softmax_ce_vs_reference_formula(n, col0, ncols):
+    """mxs_softmax_ce (the C3 step's fused loss, maxsim/cli.py:198-206) vs the float64 restatement
+    on the same scores: loss to 1e-12 relative, the fp32 gradient slice to fp32 rounding."""
+    from paper_2605_29517_b200.parallel import softmax_ce, softmax_ce_device
+
+    rng = np.random.default_rng(n + col0)
+    s = torch.from_numpy(rng.standard_normal((n, n)) * 30).cuda()
+    loss_ref, g_ref = softmax_ce(s)
+    loss, g = softmax_ce_device(s, col0, ncols)
+    assert abs(float(loss) - float(loss_ref)) <= 1e-12 * abs(float(loss_ref))
+    gr = g_ref[:, col0:col0 + ncols].to(torch.float32)
+    assert torch.allclose(g, gr, rtol=2e-7, atol=1e-30)
+    # the reference's numpy formula on the host
+    sn = s.cpu().numpy()
+    shifted = sn - sn.max(axis=1, keepdims=True)
+    lse = np.log(np.exp(shifted).sum(axis=1)) + sn.max(axis=1)
+    assert abs(float(loss) - float(np.mean(lse - np.diag(sn)))) <= 1e-12 * abs(float(loss))
