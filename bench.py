@@ -719,7 +719,7 @@ def run_c3(a, rank, world, local_rank, steps, warmup, cpu):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_29517_b200.parallel import InBatchStepGraph, inbatch_step, shard_bounds
+    from paper_2605_29517_b200.parallel import InBatchStepGraph, ShardedInBatchStepGraph, inbatch_step, shard_bounds
 
     dev = torch.device("cuda", local_rank)
     g = torch.Generator(device="cuda").manual_seed(33)
@@ -733,9 +733,16 @@ def run_c3(a, rank, world, local_rank, steps, warmup, cpu):
         fn = gstep
         path = "CUDA graph of the whole step (InBatchStepGraph): fwd (fused S4) + loss + CSR + dD + dQ"
     else:
-        def fn():
-            return inbatch_step(Q, D_loc, lo)
-        path = "parallel.inbatch_step: score all_gather, dQ all_reduce async over the dD kernel"
+        try:  # CUDA graphs around the eager NCCL collectives
+            fn = ShardedInBatchStepGraph(Q, D_loc, lo)
+            path = ("parallel.ShardedInBatchStepGraph: graphs G1 fwd | NCCL score all_gather | G2 loss + CSR + dQ | "
+                    "async NCCL dQ all_reduce over G3 dD")
+        except Exception as e:  # noqa: BLE001 -- the eager step is the same computation
+            print(f"[bench] c3 graphs unavailable ({e}); eager inbatch_step", file=sys.stderr)
+
+            def fn():
+                return inbatch_step(Q, D_loc, lo)
+            path = "parallel.inbatch_step: score all_gather, dQ all_reduce async over the dD kernel"
     ms = timed_loop(torch, dist, world, dev, steps, warmup, fn, stream)
     if rank != 0:
         return None

@@ -221,3 +221,71 @@ class InBatchStepGraph:
         """Replay: returns (loss, scores, dQ, dD) -- the graph's static output tensors."""
         self.graph.replay()
         return self.out
+
+
+class ShardedInBatchStepGraph:
+    """`inbatch_step` with B sharded over ranks, as CUDA graphs around EAGER collectives.
+
+    The local work is captured in three graphs -- G1: forward (scores + argmax); G2: loss, score
+    gradient, inverse CSR (side stream) and dQ; G3: dD -- and the two NCCL collectives run eagerly
+    between replays on static buffers (nothing collective is captured): the score all_gather
+    between G1 and G2, and the dQ all_reduce issued asynchronously right after G2 so that it
+    crosses NVLink while G3 (dD) runs.  A step is then 3 graph launches + 2 collectives instead
+    of ~20 kernel launches from Python.  With world == 1 the collectives are skipped and the
+    result equals `inbatch_step` (tests/test_gpu_parity.py).  Q / D_local are read in place.
+    """
+
+    def __init__(self, Q: torch.Tensor, D_local: torch.Tensor, doc_offset: int, group=None, warmup: int = 2):
+        import torch.distributed as dist
+
+        from .autograd import _side_stream
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.Q, self.D = Q, D_local
+        self.doc_offset = doc_offset
+        k = DeviceKernels
+        b_local, l_pad, dim = D_local.shape
+        n_q = Q.shape[0]
+        dev = Q.device
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):  # allocator warm-up (and the cached offsets) outside the captures
+                inbatch_step(Q, D_local, 0 if self.world == 1 else doc_offset, group)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.scores_full = torch.empty((n_q, b_local * self.world), dtype=torch.float64, device=dev)
+        self.gathered = torch.empty((self.world, n_q, b_local), dtype=torch.float64, device=dev)
+        self.g1, self.g2, self.g3 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g1):
+            self.scores_local, self.argmax = k.score(Q, D_local, None)
+        with torch.cuda.graph(self.g2):
+            if self.world > 1:  # the all-gathered [world, n_q, b_local] blocks -> [n_q, B]
+                self.scores_full.copy_(self.gathered.permute(1, 0, 2).reshape(n_q, -1))
+            else:
+                self.scores_full.copy_(self.scores_local)
+            main, sidec = torch.cuda.current_stream(dev), _side_stream(dev)
+            sidec.wait_stream(main)
+            with torch.cuda.stream(sidec):
+                self.csr = k.csr(self.argmax, l_pad)
+            self.loss, self.g = softmax_ce_device(self.scores_full, doc_offset if self.world > 1 else 0, b_local)
+            self.dQ = k.grad_query(D_local, self.argmax, self.g)
+            main.wait_stream(sidec)
+        with torch.cuda.graph(self.g3):
+            self.dD = k.grad_docs_csr(Q.to(D_local.dtype).contiguous(), self.argmax, self.g, self.csr,
+                                      l_pad).reshape(b_local, l_pad, dim)
+
+    def __call__(self):
+        """One step: returns (loss, scores [N_q, B], dQ all-reduced, dD_local) -- static tensors."""
+        import torch.distributed as dist
+
+        self.g1.replay()
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.gathered, self.scores_local.contiguous(), group=self.group)
+        self.g2.replay()
+        work = dist.all_reduce(self.dQ, group=self.group, async_op=True) if self.world > 1 else None
+        self.g3.replay()
+        if work is not None:
+            work.wait()
+        return self.loss, self.scores_full, self.dQ, self.dD

@@ -721,3 +721,24 @@ def test_fused_softmax_ce_vs_reference_formula(n, col0, ncols):
     shifted = sn - sn.max(axis=1, keepdims=True)
     lse = np.log(np.exp(shifted).sum(axis=1)) + sn.max(axis=1)
     assert abs(float(loss) - float(np.mean(lse - np.diag(sn)))) <= 1e-12 * abs(float(loss))
+
+
+def test_sharded_step_graphs_equal_eager_step():
+    """ShardedInBatchStepGraph (G1 forward | eager all_gather | G2 loss + CSR + dQ | eager async
+    all_reduce | G3 dD) at world 1 reproduces inbatch_step bit for bit, replay after replay, and
+    follows in-place updates of Q / D."""
+    from paper_2605_29517_b200.parallel import ShardedInBatchStepGraph, inbatch_step
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Q = torch.randn(8, 300, 128, device="cuda", generator=g).bfloat16()
+    D = torch.randn(8, 260, 128, device="cuda", generator=g).bfloat16()
+    step = ShardedInBatchStepGraph(Q, D, 0)
+    for it in range(3):
+        if it == 2:  # in-place parameter update between steps
+            Q.mul_(-0.5)
+            D.add_(0.25)
+        loss, scores, dQ, dD = step()
+        rl, rs, rq, rd = inbatch_step(Q, D, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(scores, rs) and torch.equal(loss, rl)
+        assert torch.equal(dQ, rq) and torch.equal(dD, rd)
