@@ -282,7 +282,7 @@ class ShardedInBatchStepGraph:
 
         self.g1.replay()
         if self.world > 1:
-            dist.all_gather_into_tensor(self.gathered, self.scores_local.contiguous(), group=self.group)
+            dist.all_gather(list(self.gathered.unbind(0)), self.scores_local.contiguous(), group=self.group)
         self.g2.replay()
         work = dist.all_reduce(self.dQ, group=self.group, async_op=True) if self.world > 1 else None
         self.g3.replay()

@@ -7,6 +7,8 @@ Tolerances (BASELINE.json north_star):
   * gradients: within 1e-3 relative (max-norm) of the float64 oracle.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -742,3 +744,42 @@ def test_sharded_step_graphs_equal_eager_step():
         torch.cuda.synchronize()
         assert torch.equal(scores, rs) and torch.equal(loss, rl)
         assert torch.equal(dQ, rq) and torch.equal(dD, rd)
+
+
+def _sharded_graph_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2605_29517_b200.parallel import ShardedInBatchStepGraph, inbatch_step
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    Q = torch.randn(8, 200, 128, device="cuda", generator=g).bfloat16()
+    D = torch.randn(8, 150, 128, device="cuda", generator=g).bfloat16()
+    lo, hi = 4 * rank, 4 * rank + 4
+    D_loc = D[lo:hi].contiguous()
+    step = ShardedInBatchStepGraph(Q, D_loc, lo)
+    ok = True
+    for _ in range(2):
+        loss, scores, dQ, dD = step()
+        rl, rs, rq, rd = inbatch_step(Q, D_loc, lo)
+        torch.cuda.synchronize()
+        ok &= bool(torch.equal(scores, rs) and torch.equal(loss, rl) and torch.equal(dQ, rq) and torch.equal(dD, rd))
+    out[rank] = ok
+    dist.destroy_process_group()
+
+
+def test_sharded_step_graphs_two_ranks_equal_eager():
+    """World 2 (two processes on cuda:0 over gloo, B sharded 4 + 4): the graph step with the
+    eager all_gather / async all_reduce between replays equals the eager sharded step bit for bit."""
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = tmp.Manager().dict()
+    tmp.spawn(_sharded_graph_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] and out[1]
